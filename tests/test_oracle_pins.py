@@ -1,0 +1,286 @@
+"""Pins of the fp64 oracle against things other than itself (CPU only).
+
+Each test names the pin from SURVEY.md 8(c) / DESIGN.md "Oracle pins" it
+implements.  A plausible mistake in oracle/ (a transposed axis, a missing
+scale, a wrong residual, a softmax over the wrong axis) fails at least one.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "hand_examples.json")
+RNG = np.random.default_rng(20260418)
+
+
+def rand(*shape, scale=1.0):
+    return RNG.normal(0.0, scale, shape)
+
+
+SHAPES = [(3, 4, 2, 4), (1, 5, 1, 3), (4, 1, 2, 2), (2, 3, 1, 8), (5, 6, 3, 2)]
+
+
+# --- I1: block-mask equivalence with joint attention over all K*N tokens ----
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_I1_temporal_equals_joint_under_temporal_mask(shape):
+    q, k, v = rand(*shape), rand(*shape), rand(*shape)
+    K, N = shape[:2]
+    ref = oracle.joint_masked(q, k, v, oracle.mask_temporal(K, N))
+    np.testing.assert_allclose(oracle.temporal(q, k, v), ref, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_I1_spatial_equals_joint_under_spatial_mask(shape):
+    q, k, v = rand(*shape), rand(*shape), rand(*shape)
+    K, N = shape[:2]
+    ref = oracle.joint_masked(q, k, v, oracle.mask_spatial(K, N))
+    np.testing.assert_allclose(oracle.spatial(q, k, v), ref, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_I1_block_equals_masked_joint_composition(shape):
+    x = rand(*shape)
+    K, N = shape[:2]
+    xt = x + oracle.joint_masked(x, x, x, oracle.mask_temporal(K, N))
+    ref = xt + oracle.joint_masked(xt, xt, xt, oracle.mask_spatial(K, N))
+    np.testing.assert_allclose(oracle.block(x), ref, rtol=0, atol=1e-12)
+
+
+def test_joint_unmasked_matches_brute_force_loops():
+    """Tiny brute force with math.exp loops (independent of numpy's matmul)."""
+    K, N, H, d = 2, 2, 1, 3
+    q, k, v = rand(K, N, H, d), rand(K, N, H, d), rand(K, N, H, d)
+    toks = [(t, n) for t in range(K) for n in range(N)]
+    out = np.zeros_like(q)
+    for h in range(H):
+        for (t, n) in toks:
+            w = [math.exp(sum(q[t, n, h, i] * k[a, b, h, i] for i in range(d)) / math.sqrt(d))
+                 for (a, b) in toks]
+            z = sum(w)
+            for i in range(d):
+                out[t, n, h, i] = sum(wj * v[a, b, h, i] for wj, (a, b) in zip(w, toks)) / z
+    np.testing.assert_allclose(oracle.joint_masked(q, k, v), out, rtol=0, atol=1e-12)
+
+
+# --- library routine: torch SDPA in fp64 on CPU -----------------------------
+
+def sdpa(q, k, v):
+    """[G, L, d] fp64 through torch.nn.functional.scaled_dot_product_attention."""
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a))[None]
+    return torch.nn.functional.scaled_dot_product_attention(t(q), t(k), t(v))[0].numpy()
+
+
+@pytest.mark.parametrize("shape", [(6, 7, 3, 16), (1, 33, 2, 32), (9, 1, 2, 64)])
+def test_temporal_matches_library_sdpa(shape):
+    q, k, v = rand(*shape), rand(*shape), rand(*shape)
+    K, N, H, d = shape
+    g = lambda a: a.transpose(1, 2, 0, 3).reshape(N * H, K, d)
+    ref = sdpa(g(q), g(k), g(v)).reshape(N, H, K, d).transpose(2, 0, 1, 3)
+    np.testing.assert_allclose(oracle.temporal(q, k, v), ref, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("shape", [(6, 7, 3, 16), (2, 65, 2, 32), (1, 40, 1, 64)])
+def test_spatial_matches_library_sdpa(shape):
+    q, k, v = rand(*shape), rand(*shape), rand(*shape)
+    K, N, H, d = shape
+    g = lambda a: a.transpose(0, 2, 1, 3).reshape(K * H, N, d)
+    ref = sdpa(g(q), g(k), g(v)).reshape(K, H, N, d).transpose(0, 2, 1, 3)
+    np.testing.assert_allclose(oracle.spatial(q, k, v), ref, rtol=0, atol=1e-12)
+
+
+# --- I2 / I3: degenerate sizes ---------------------------------------------
+
+def test_I2_K1_temporal_is_identity_on_v_exactly():
+    q, k, v = rand(1, 9, 2, 8), rand(1, 9, 2, 8), rand(1, 9, 2, 8)
+    assert np.array_equal(oracle.temporal(q, k, v), v)
+
+
+def test_I3_N1_spatial_is_identity_on_v_exactly():
+    q, k, v = rand(7, 1, 2, 8), rand(7, 1, 2, 8), rand(7, 1, 2, 8)
+    assert np.array_equal(oracle.spatial(q, k, v), v)
+
+
+def test_I2_K1_block_closed_form():
+    """K=1: X_t = x + x = 2x, y = 2x + SDPA(2x) per head (library routine)."""
+    x = rand(1, 11, 2, 8)
+    xt = 2 * x
+    g = xt[0].transpose(1, 0, 2)                      # [h][n][d]
+    ref = xt + sdpa(g, g, g).transpose(1, 0, 2)[None]
+    np.testing.assert_allclose(oracle.block(x), ref, rtol=0, atol=1e-12)
+
+
+# --- I4: permutation equivariance ------------------------------------------
+
+@pytest.mark.parametrize("fn", ["temporal", "spatial"])
+def test_I4_permutation_equivariance(fn):
+    f = getattr(oracle, fn)
+    q, k, v = rand(5, 6, 2, 4), rand(5, 6, 2, 4), rand(5, 6, 2, 4)
+    pn, pk = RNG.permutation(6), RNG.permutation(5)
+    base = f(q, k, v)
+    np.testing.assert_allclose(f(q[:, pn], k[:, pn], v[:, pn]), base[:, pn], atol=1e-12, rtol=0)
+    np.testing.assert_allclose(f(q[pk], k[pk], v[pk]), base[pk], atol=1e-12, rtol=0)
+
+
+def test_I4_block_permutation_equivariance():
+    x = rand(4, 6, 2, 4)
+    pn, pk = RNG.permutation(6), RNG.permutation(4)
+    base = oracle.block(x)
+    np.testing.assert_allclose(oracle.block(x[:, pn]), base[:, pn], atol=1e-12, rtol=0)
+    np.testing.assert_allclose(oracle.block(x[pk]), base[pk], atol=1e-12, rtol=0)
+
+
+def test_I4_heads_are_independent():
+    x = rand(3, 5, 3, 4)
+    y = oracle.block(x)
+    for h in range(3):
+        np.testing.assert_allclose(oracle.block(x[:, :, h:h + 1]), y[:, :, h:h + 1], atol=1e-12, rtol=0)
+
+
+# --- I5: softmax rows sum to one -------------------------------------------
+
+def test_I5_rows_sum_to_one():
+    q, k, v = rand(4, 37, 8, scale=3.0), rand(4, 37, 8, scale=3.0), rand(4, 37, 8)
+    _, P = oracle.attend(q, k, v, return_p=True)
+    assert np.max(np.abs(P.sum(-1) - 1.0)) <= 1e-13
+    assert np.all(P >= 0)
+
+
+# --- I6: closed forms -------------------------------------------------------
+
+def test_I6_zero_query_gives_mean_of_v():
+    k, v = rand(4, 5, 2, 8), rand(4, 5, 2, 8)
+    q = np.zeros_like(k)
+    np.testing.assert_allclose(oracle.temporal(q, k, v), np.broadcast_to(v.mean(0, keepdims=True), v.shape), atol=1e-12, rtol=0)
+    np.testing.assert_allclose(oracle.spatial(q, k, v), np.broadcast_to(v.mean(1, keepdims=True), v.shape), atol=1e-12, rtol=0)
+
+
+def test_I6_equal_keys_give_mean_of_v():
+    q, v = rand(4, 5, 2, 8), rand(4, 5, 2, 8)
+    kt = np.broadcast_to(rand(1, 5, 2, 8), q.shape).copy()      # same key on every frame
+    np.testing.assert_allclose(oracle.temporal(q, kt, v), np.broadcast_to(v.mean(0, keepdims=True), v.shape), atol=1e-12, rtol=0)
+
+
+def test_I6_identical_frames_temporal_returns_frame():
+    """All frames identical -> softmax uniform over equal keys -> x[0]."""
+    f = rand(1, 6, 2, 8)
+    x = np.repeat(f, 5, axis=0)
+    np.testing.assert_allclose(oracle.temporal(x, x, x), x, atol=1e-12, rtol=0)
+
+
+def test_I6_key_shift_invariance():
+    q, k, v = rand(4, 5, 2, 8), rand(4, 5, 2, 8), rand(4, 5, 2, 8)
+    # temporal: a shift constant along the frame axis adds a per-row constant to S
+    c_t = rand(1, 5, 2, 8)
+    np.testing.assert_allclose(oracle.temporal(q, k + c_t, v), oracle.temporal(q, k, v), atol=1e-11, rtol=0)
+    c_s = rand(4, 1, 2, 8)
+    np.testing.assert_allclose(oracle.spatial(q, k + c_s, v), oracle.spatial(q, k, v), atol=1e-11, rtol=0)
+
+
+def test_I6_linear_in_v_and_convex():
+    q, k, v1, v2 = (rand(4, 6, 2, 8) for _ in range(4))
+    for f in (oracle.temporal, oracle.spatial):
+        np.testing.assert_allclose(f(q, k, 2.0 * v1 - 3.0 * v2), 2.0 * f(q, k, v1) - 3.0 * f(q, k, v2), atol=1e-11, rtol=0)
+    o = oracle.temporal(q, k, v1)
+    assert np.all(o <= v1.max(0, keepdims=True) + 1e-12) and np.all(o >= v1.min(0, keepdims=True) - 1e-12)
+    o = oracle.spatial(q, k, v1)
+    assert np.all(o <= v1.max(1, keepdims=True) + 1e-12) and np.all(o >= v1.min(1, keepdims=True) - 1e-12)
+
+
+# --- I7: large-logit limit ---------------------------------------------------
+
+def test_I7_large_logit_selects_argmax():
+    K, N, H, d = 1, 7, 1, 4
+    k = rand(K, N, H, d)
+    v = rand(K, N, H, d)
+    q = np.broadcast_to(k[:, 3:4], k.shape) * 1e3       # argmax key is n=3 for every query
+    o = oracle.spatial(q, k, v)
+    np.testing.assert_allclose(o, np.broadcast_to(v[:, 3:4], v.shape), atol=1e-9, rtol=0)
+
+
+# --- golden, hand-derived (tests/golden/hand_examples.json) ------------------
+
+def golden():
+    with open(GOLDEN) as f:
+        return json.load(f)
+
+
+def test_golden_temporal_k2():
+    g = golden()["temporal_k2"]
+    o = oracle.temporal(*(np.array(g[n], dtype=np.float64) for n in "qkv"))
+    np.testing.assert_allclose(o, np.array(g["out"]), atol=1e-15, rtol=0)
+
+
+def test_golden_spatial_n3():
+    g = golden()["spatial_n3"]
+    o = oracle.spatial(*(np.array(g[n], dtype=np.float64) for n in "qkv"))
+    np.testing.assert_allclose(o, np.array(g["out"]), atol=g["tol"], rtol=0)
+
+
+def test_golden_block_k2_n1():
+    g = golden()["block_k2_n1"]
+    y = oracle.block(np.array(g["x"], dtype=np.float64))
+    np.testing.assert_allclose(y, np.array(g["y"]), atol=g["tol"], rtol=0)
+
+
+def test_I8_flop_model_spec_example():
+    g = golden()["flops_spec_example"]
+    assert oracle.flops_spec_convention(g["K"], g["N"], g["d"]) == g["spec_flops"]
+    assert oracle.flops_tsf(g["K"], g["N"], 1, g["d"]) == g["tsf_flops_H1"]
+
+
+def test_I8_flop_model_counts_matmul_macs():
+    """Count the multiply-adds the oracle's matmuls perform, by shape."""
+    K, N, H, d = 3, 5, 2, 4
+    macs = H * (N * (K * K * d + K * K * d) + K * (N * N * d + N * N * d))
+    assert oracle.flops_tsf(K, N, H, d) == 2 * macs
+
+
+# --- sampled-row evaluation equals the full oracle -------------------------
+
+def test_sampled_rows_match_full():
+    K, N, H, d = 4, 9, 3, 8
+    q, k, v, x = (rand(K, N, H, d) for _ in range(4))
+    rows = [(0, 0, 0), (3, 8, 2), (1, 4, 1), (2, 7, 0)]
+    T, S, B = oracle.temporal(q, k, v), oracle.spatial(q, k, v), oracle.block(x)
+    pick = lambda a: np.array([a[t, n, h] for t, n, h in rows])
+    np.testing.assert_allclose(oracle.temporal_rows(q, k, v, rows), pick(T), atol=1e-12, rtol=0)
+    np.testing.assert_allclose(oracle.spatial_rows(q, k, v, rows), pick(S), atol=1e-12, rtol=0)
+    np.testing.assert_allclose(oracle.block_rows(x, rows), pick(B), atol=1e-12, rtol=0)
+    np.testing.assert_allclose(oracle.block_plane(x, 2, 1), B[2, :, 1], atol=1e-12, rtol=0)
+
+
+# --- distributed semantics: reshard is a pure permutation ------------------
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_reshard_is_index_permutation(P):
+    a = rand(8, 12, 2, 4)
+    tok = [oracle.shard_tokens(a, P, p) for p in range(P)]
+    fr = oracle.reshard_t2s(tok)
+    for p in range(P):
+        assert np.array_equal(fr[p], a[p * 8 // P:(p + 1) * 8 // P])
+    back = oracle.reshard_s2t(fr)
+    for p in range(P):
+        assert np.array_equal(back[p], tok[p])
+
+
+def test_sharded_block_equals_block():
+    """O5: temporal on token shards, reshard, spatial on frame shards == block."""
+    x = rand(4, 6, 2, 4)
+    P = 2
+    xt = [s + oracle.temporal(s, s, s) for s in (oracle.shard_tokens(x, P, p) for p in range(P))]
+    fr = oracle.reshard_t2s(xt)
+    y = np.concatenate([f + oracle.spatial(f, f, f) for f in fr], axis=0)
+    np.testing.assert_allclose(y, oracle.block(x), atol=1e-12, rtol=0)
+
+
+def test_oracle_rejects_non_finite():
+    q = rand(2, 3, 1, 4)
+    q[0, 0, 0, 0] = np.nan
+    with pytest.raises(ValueError):
+        oracle.temporal(q, q, q)
