@@ -1,0 +1,140 @@
+/*
+ * tsf.h -- C ABI of libtsf.so: TimeSformer-style factorized ("divided")
+ * space-time attention on NVIDIA B200 (sm_100a).
+ *
+ * What it computes (Sec. I): "temporal attention at each
+ * spatial location ... followed by spatial attention at each time frame",
+ * per-layer cost O(K^2 N + K N^2) (Fig. 1 caption, Table I), in
+ * place of joint attention over all K*N tokens.  A token is one
+ * spatial patch of one frame; K frames x N tokens per frame.
+ *
+ * Layout.  Every tensor is row-major [K, N, H, d] (frames, tokens per frame,
+ * heads, head dim; d fastest), contiguous, in device memory unless the
+ * function name ends in _host.  bf16 tensors are passed as tsf_bf16 (the raw
+ * 16-bit pattern, e.g. torch.bfloat16 storage).  The softmax scale is
+ * 1/sqrt(d) (reading G4); there are no projections (reading G1).
+ *
+ * Ownership.  The caller owns every input/output buffer; they must be
+ * 16-byte aligned and outputs must not overlap inputs.  The handle owns its
+ * workspace (allocated in tsf_create*, no allocation in the call path except
+ * the one-time staging buffers of tsf_spacetime_block_host) and, for
+ * distributed handles, its NCCL communicator.
+ *
+ * Streams.  `stream` is a cudaStream_t (NULL = legacy default stream).  All
+ * calls are asynchronous on that stream, except tsf_spacetime_block_host which
+ * synchronises it before returning.  A handle is not thread-safe; use one
+ * handle per stream.  Results are deterministic: the same inputs give the same
+ * bits on every run.
+ *
+ * Errors.  Arguments are validated synchronously before anything is enqueued;
+ * no exception crosses the ABI.  tsf_last_error() describes the last failure
+ * of a handle (or of handle creation when called with NULL).
+ */
+#ifndef TSF_H_
+#define TSF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef uint16_t tsf_bf16;            /* bf16 bit pattern */
+typedef struct tsf_handle tsf_handle; /* opaque */
+
+typedef enum {
+  TSF_OK = 0,
+  TSF_ERR_CONFIG = 2,      /* bad size, null/misaligned/aliased pointer, K%P or N%P != 0 */
+  TSF_ERR_NUMERIC = 3,     /* reserved: non-finite input (debug builds only) */
+  TSF_ERR_UNSUPPORTED = 4, /* d not in {32, 64, 128}, or device is not sm_100 */
+  TSF_ERR_CUDA = 5,        /* CUDA runtime/driver failure (launch, copy, tensor map) */
+  TSF_ERR_NCCL = 6,        /* NCCL failure */
+  TSF_ERR_NOMEM = 7        /* workspace allocation failed */
+} tsf_status;
+
+enum { TSF_T2S = 0, TSF_S2T = 1 }; /* reshard directions */
+
+/* Create a single-GPU handle for a [K, N, H, d] layer on the current CUDA
+ * device.  K, N, H >= 1; d in {32, 64, 128}.  Allocates the block workspace
+ * (X_t as two bf16 planes, 4*K*N*H*d bytes). */
+tsf_status tsf_create(int K, int N, int H, int d, tsf_handle** out);
+
+/* Temporal attention ("at each spatial location"): for every (n, h),
+ *   o[t,n,h,:] = sum_t' softmax_t'(<q[t,n,h,:], k[t',n,h,:]> / sqrt(d)) v[t',n,h,:].
+ * q, k, v, o: bf16 [K, Nl, H, d] with Nl = N (single GPU) or N/P (distributed
+ * handle: the rank's token shard).  Accumulation in fp32; o rounded to bf16. */
+tsf_status tsf_temporal_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v,
+                             tsf_bf16* o, void* stream);
+
+/* Spatial attention ("at each time frame"): for every (t, h),
+ *   o[t,n,h,:] = sum_n' softmax_n'(<q[t,n,h,:], k[t,n',h,:]> / sqrt(d)) v[t,n',h,:].
+ * q, k, v, o: bf16 [Kl, N, H, d] with Kl = K or K/P (the rank's frame shard). */
+tsf_status tsf_spatial_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v,
+                            tsf_bf16* o, void* stream);
+
+/* Divided space-time block, temporal then spatial ("followed by"), with
+ * identity projections and residual weight 1 (readings G1, G5):
+ *   X_t = x + T(x, x, x);   y = X_t + S(X_t, X_t, X_t).
+ * x: bf16.  y: fp32.  X_t is kept as bf16 hi + bf16 lo (X_t = hi + lo to
+ * ~2^-17 relative); the MMAs read hi, the residual adds hi + lo (reading G8).
+ * Single GPU: x, y are [K, N, H, d].  Distributed: x is the token shard
+ * [K, N/P, H, d], y the frame shard [K/P, N, H, d]; one all-to-all (NCCL,
+ * bytes, bit-exact) reshards X_t between the stages. */
+tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void* stream);
+
+/* Same as tsf_spacetime_block with HOST buffers (pinned memory recommended):
+ * copies x host->device, runs the block, copies y device->host and
+ * synchronises `stream`.  Staging buffers are allocated on first use. */
+tsf_status tsf_spacetime_block_host(tsf_handle* h, const tsf_bf16* x_host, float* y_host, void* stream);
+
+/* Release the workspace (and the NCCL communicator of a distributed handle;
+ * aborted instead of destroyed if it reports an asynchronous error). */
+void tsf_destroy(tsf_handle* h);
+
+/* ---- distributed (one process per GPU, NCCL over NVLink/NVSwitch) ---- */
+
+/* Fill id128 (128 bytes) with a new NCCL unique id.  Call on rank 0 and
+ * broadcast the bytes to the other ranks (the Python binding uses the torch
+ * process group). */
+tsf_status tsf_get_unique_id(void* id128);
+
+/* Collective over `world` ranks: create a distributed handle on the current
+ * device.  Requires K % world == 0 and N % world == 0. */
+tsf_status tsf_create_dist(int K, int N, int H, int d, const void* id128, int rank, int world,
+                           tsf_handle** out);
+
+/* Reshard a bf16 tensor between the two shardings (pure data movement,
+ * bit-exact): TSF_T2S: in = token shard [K, N/P, H, d] -> out = frame shard
+ * [K/P, N, H, d]; TSF_S2T: the inverse.  Collective over all ranks. */
+tsf_status tsf_reshard(tsf_handle* h, int dir, const tsf_bf16* in, tsf_bf16* out, void* stream);
+
+/* ---- layout kernels (HBM-bound, 16-byte vectors) ---- */
+
+/* Frame-major <-> token-major transpose of a bf16 [A, B, H, d] tensor into
+ * [B, A, H, d] (A = K, B = N for frame->token; swap for the inverse).  The
+ * attention kernels read both orders directly through TMA views, so the block
+ * never needs it; it is exported for callers whose data is token-major. */
+tsf_status tsf_transpose(tsf_handle* h, int A, int B, const tsf_bf16* in, tsf_bf16* out, void* stream);
+
+/* ---- introspection ---- */
+
+/* Last error message of h (or of the last failed create when h is NULL). */
+const char* tsf_last_error(const tsf_handle* h);
+
+/* Number of kernels the last tsf_* compute call launched (bench accounting). */
+int tsf_last_launch_count(const tsf_handle* h);
+
+/* Stage timing with CUDA events recorded on the call's stream around each
+ * stage's kernel(s).  tsf_set_timing(h, 1) starts recording (clearing earlier
+ * records), 0 stops.  tsf_stage_ms synchronises on the recorded events and
+ * returns the summed milliseconds and the number of recorded launches of
+ * stage 0 = temporal attention, 1 = spatial attention, 2 = reshard
+ * (all-to-all + unpack), 3 = host<->device copies. */
+tsf_status tsf_set_timing(tsf_handle* h, int enable);
+tsf_status tsf_stage_ms(tsf_handle* h, int stage, float* total_ms, int* n_records);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSF_H_ */

@@ -1,0 +1,238 @@
+"""B200-native factorized (divided) space-time attention -- Python binding.
+
+Thin ctypes binding over libtsf.so (C ABI in include/tsf.h).  Argument
+marshalling only: every step of the path runs in the library's sm_100a
+kernels; PyTorch provides device memory, streams and process groups.  There is
+no CPU fallback: if libtsf.so is missing or the device is not a B200 the calls
+raise.
+
+    import paper_2604_16590_b200 as tsf
+    layer = tsf.Layer(K, N, H, d)            # single GPU
+    y = layer.block(x)                       # x: bf16 [K, N, H, d] -> y: fp32
+    o = layer.temporal(q, k, v); o = layer.spatial(q, k, v)
+
+Distributed (one process per GPU, torch.distributed initialised):
+    layer = tsf.Layer(K, N, H, d, group=torch.distributed.group.WORLD)
+    y_frames = layer.block(x_tokens)         # [K, N/P, H, d] -> [K/P, N, H, d]
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtsf.so")
+
+# status codes (include/tsf.h)
+TSF_OK, TSF_ERR_CONFIG, TSF_ERR_NUMERIC, TSF_ERR_UNSUPPORTED, TSF_ERR_CUDA, TSF_ERR_NCCL, TSF_ERR_NOMEM = \
+    0, 2, 3, 4, 5, 6, 7
+STATUS_NAMES = {0: "TSF_OK", 2: "TSF_ERR_CONFIG", 3: "TSF_ERR_NUMERIC", 4: "TSF_ERR_UNSUPPORTED",
+                5: "TSF_ERR_CUDA", 6: "TSF_ERR_NCCL", 7: "TSF_ERR_NOMEM"}
+TSF_T2S, TSF_S2T = 0, 1
+STAGE_TEMPORAL, STAGE_SPATIAL, STAGE_RESHARD, STAGE_COPY, STAGE_TRANSPOSE = 0, 1, 2, 3, 4
+
+# Every function declared in include/tsf.h: (name, restype, argtypes)
+_P, _I, _F = ctypes.c_void_p, ctypes.c_int, ctypes.c_float
+SIGNATURES = [
+    ("tsf_create", _I, [_I, _I, _I, _I, ctypes.POINTER(_P)]),
+    ("tsf_temporal_attn", _I, [_P, _P, _P, _P, _P, _P]),
+    ("tsf_spatial_attn", _I, [_P, _P, _P, _P, _P, _P]),
+    ("tsf_spacetime_block", _I, [_P, _P, _P, _P]),
+    ("tsf_spacetime_block_host", _I, [_P, _P, _P, _P]),
+    ("tsf_destroy", None, [_P]),
+    ("tsf_get_unique_id", _I, [_P]),
+    ("tsf_create_dist", _I, [_I, _I, _I, _I, _P, _I, _I, ctypes.POINTER(_P)]),
+    ("tsf_reshard", _I, [_P, _I, _P, _P, _P]),
+    ("tsf_transpose", _I, [_P, _I, _I, _P, _P, _P]),
+    ("tsf_last_error", ctypes.c_char_p, [_P]),
+    ("tsf_last_launch_count", _I, [_P]),
+    ("tsf_set_timing", _I, [_P, _I]),
+    ("tsf_stage_ms", _I, [_P, _I, ctypes.POINTER(_F), ctypes.POINTER(_I)]),
+]
+
+_lib = None
+
+
+class TsfError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def lib() -> ctypes.CDLL:
+    """Load libtsf.so (raises if it has not been built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run `python -m paper_2604_16590_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+        for name, res, args in SIGNATURES:
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int, handle=None):
+    if status != TSF_OK:
+        msg = lib().tsf_last_error(handle)
+        raise TsfError(status, msg.decode() if msg else "")
+
+
+def _stream_ptr(stream=None) -> int:
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def _need(t, dtype, shape, name):
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+class Layer:
+    """One factorized space-time attention layer of shape [K, N, H, d].
+
+    group: a torch.distributed process group for the multi-GPU path (one
+    process per GPU); None = single GPU.
+    """
+
+    def __init__(self, K: int, N: int, H: int, d: int, group=None):
+        self.K, self.N, self.H, self.d = K, N, H, d
+        self._h = ctypes.c_void_p()
+        L = lib()
+        if group is None:
+            self.world, self.rank = 1, 0
+            _check(L.tsf_create(K, N, H, d, ctypes.byref(self._h)))
+        else:
+            import torch
+            import torch.distributed as dist
+            self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+            uid = (ctypes.c_char * 128)()
+            if self.rank == 0:
+                _check(L.tsf_get_unique_id(uid))
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8)
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda()
+            dist.broadcast(t, src=dist.get_global_rank(group, 0), group=group)
+            raw = bytes(t.cpu().tolist())
+            uid = (ctypes.c_char * 128).from_buffer_copy(raw)
+            _check(L.tsf_create_dist(K, N, H, d, uid, self.rank, self.world, ctypes.byref(self._h)))
+
+    # shapes of the shards this rank holds
+    @property
+    def token_shard_shape(self):
+        return (self.K, self.N // self.world, self.H, self.d)
+
+    @property
+    def frame_shard_shape(self):
+        return (self.K // self.world, self.N, self.H, self.d)
+
+    def close(self):
+        if self._h:
+            lib().tsf_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ---- compute ----
+    def temporal(self, q, k, v, out=None, stream=None):
+        """tsf_temporal_attn: q, k, v bf16 [K, N/P, H, d] -> bf16 (P:64 temporal)."""
+        import torch
+        shp = self.token_shard_shape
+        for t, n in ((q, "q"), (k, "k"), (v, "v")):
+            _need(t, torch.bfloat16, shp, n)
+        out = torch.empty_like(q) if out is None else out
+        _need(out, torch.bfloat16, shp, "out")
+        _check(lib().tsf_temporal_attn(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                       _stream_ptr(stream)), self._h)
+        return out
+
+    def spatial(self, q, k, v, out=None, stream=None):
+        """tsf_spatial_attn: q, k, v bf16 [K/P, N, H, d] -> bf16 (P:64 spatial)."""
+        import torch
+        shp = self.frame_shard_shape
+        for t, n in ((q, "q"), (k, "k"), (v, "v")):
+            _need(t, torch.bfloat16, shp, n)
+        out = torch.empty_like(q) if out is None else out
+        _need(out, torch.bfloat16, shp, "out")
+        _check(lib().tsf_spatial_attn(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                      _stream_ptr(stream)), self._h)
+        return out
+
+    def block(self, x, out=None, stream=None):
+        """tsf_spacetime_block: x bf16 token shard -> y fp32 frame shard."""
+        import torch
+        _need(x, torch.bfloat16, self.token_shard_shape, "x")
+        out = torch.empty(self.frame_shard_shape, dtype=torch.float32, device=x.device) if out is None else out
+        _need(out, torch.float32, self.frame_shard_shape, "out")
+        _check(lib().tsf_spacetime_block(self._h, x.data_ptr(), out.data_ptr(), _stream_ptr(stream)), self._h)
+        return out
+
+    def block_host(self, x_host, y_host, stream=None):
+        """tsf_spacetime_block_host: CPU (pinned) bf16 x -> CPU fp32 y, copies included."""
+        import torch
+        _need(x_host, torch.bfloat16, self.token_shard_shape, "x_host")
+        _need(y_host, torch.float32, self.frame_shard_shape, "y_host")
+        if x_host.is_cuda or y_host.is_cuda:
+            raise ValueError("block_host takes host tensors")
+        _check(lib().tsf_spacetime_block_host(self._h, x_host.data_ptr(), y_host.data_ptr(), _stream_ptr(stream)),
+               self._h)
+        return y_host
+
+    def reshard(self, x, direction: int, out=None, stream=None):
+        """tsf_reshard: TSF_T2S token shard -> frame shard, TSF_S2T the inverse (bit-exact)."""
+        import torch
+        src, dst = ((self.token_shard_shape, self.frame_shard_shape) if direction == TSF_T2S
+                    else (self.frame_shard_shape, self.token_shard_shape))
+        _need(x, torch.bfloat16, src, "x")
+        out = torch.empty(dst, dtype=torch.bfloat16, device=x.device) if out is None else out
+        _need(out, torch.bfloat16, dst, "out")
+        _check(lib().tsf_reshard(self._h, direction, x.data_ptr(), out.data_ptr(), _stream_ptr(stream)), self._h)
+        return out
+
+    def transpose(self, x, out=None, stream=None):
+        """tsf_transpose: bf16 [A, B, H, d] -> [B, A, H, d] (frame-major <-> token-major)."""
+        import torch
+        A, B = x.shape[0], x.shape[1]
+        _need(x, torch.bfloat16, (A, B, self.H, self.d), "x")
+        out = torch.empty((B, A, self.H, self.d), dtype=torch.bfloat16, device=x.device) if out is None else out
+        _need(out, torch.bfloat16, (B, A, self.H, self.d), "out")
+        _check(lib().tsf_transpose(self._h, A, B, x.data_ptr(), out.data_ptr(), _stream_ptr(stream)), self._h)
+        return out
+
+    # ---- accounting ----
+    def last_launch_count(self) -> int:
+        return lib().tsf_last_launch_count(self._h)
+
+    def set_timing(self, enable: bool):
+        _check(lib().tsf_set_timing(self._h, 1 if enable else 0), self._h)
+
+    def stage_ms(self, stage: int):
+        ms, n = ctypes.c_float(), ctypes.c_int()
+        _check(lib().tsf_stage_ms(self._h, stage, ctypes.byref(ms), ctypes.byref(n)), self._h)
+        return ms.value, n.value
+
+
+def flops(K: int, N: int, H: int, d: int) -> int:
+    """Algorithmic flops of one layer: 4 H d (K N^2 + N K^2) (QK^T + PV)."""
+    return 4 * H * d * (K * N * N + N * K * K)

@@ -1,0 +1,267 @@
+// Flash (online-softmax) attention for long sequences (L > 128): spatial
+// attention over N tokens of each frame (C2-C5) and temporal attention over
+// K = 1024 frames (C5).  Tensor-core bound: 4 d L^2 flops per group against
+// 8 d L bytes.
+//
+// One CTA owns two 128-row query tiles of one group and streams the group's
+// K/V in 128-row tiles through an NST-deep TMA ring shared by both query tiles
+// (halves K/V smem/L2 traffic per flop).  The MMA warp ping-pongs
+// S_t = Q_t K_j^T and O_t += P_t V_j between the two tiles so the tensor core
+// works on one tile while the softmax warpgroup of the other runs.
+//
+// TMEM (512 columns): S0 [0,128), S1 [128,256), O0 [256,256+D), O1 after it.
+// P_t (bf16 pairs, 64 columns) overwrites the upper half of S_t after S_t has
+// been read into registers.  Online softmax in the log2 domain with
+// conditional rescaling: the running max is only moved (and O_t rescaled in
+// TMEM) when a row max grows by more than RESCALE_LOG2; the final O/l is exact
+// either way because l is accumulated against the same stale max.
+//
+// Warp roles (320 threads): warps 0-3 softmax of tile 0, warps 4-7 softmax of
+// tile 1 (thread owns TMEM lane = tile row), warp 8 TMA producer, warp 9 MMA
+// issuer and TMEM owner.
+#pragma once
+#include "sm100.cuh"
+#include "attn_common.cuh"
+
+namespace tsf {
+
+constexpr float RESCALE_LOG2 = 8.0f;
+
+template <int D, int EPI, int NST>
+struct FlashCfg {
+  static constexpr int SWB = (2 * D < 128) ? 2 * D : 128;
+  static constexpr int CH = SWB / 2;
+  static constexpr int NCH = D / CH;
+  static constexpr int CHUNK_BYTES = 128 * SWB;
+  static constexpr int TILE_BYTES = NCH * CHUNK_BYTES;  // 128 x D bf16
+  static constexpr int Q_BYTES = 2 * TILE_BYTES;
+  static constexpr int STAGE_BYTES = 2 * TILE_BYTES;    // K + V
+  static constexpr int SMEM = Q_BYTES + NST * STAGE_BYTES + 1024 + 256;
+  static constexpr int THREADS = 320;
+  static constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 256 + D;
+};
+
+template <int D, int EPI, int NST>
+__global__ void __launch_bounds__(320, 1)
+attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                  const __grid_constant__ CUtensorMap tv, const AttnParams p) {
+  using C = FlashCfg<D, EPI, NST>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                        // Q0 | Q1
+  uint8_t* sKV = smem + C::Q_BYTES;          // NST x (K | V)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + NST * C::STAGE_BYTES);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;               // [NST]
+  uint64_t* v_full = k_full + NST;           // [NST]
+  uint64_t* kv_empty = v_full + NST;         // [NST]
+  uint64_t* s_full = kv_empty + NST;         // [2]
+  uint64_t* p_full = s_full + 2;             // [2]
+  uint64_t* o_full = p_full + 2;             // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 2);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int L = p.L, nkv = p.nkv;
+  const int qp = blockIdx.x % p.n_qpairs;
+  const int grp = blockIdx.x / p.n_qpairs;
+  const int ga = grp % p.A, gb = grp / p.A;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 4);
+      mbar_init(&o_full[t], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc<512>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 8) {
+    // ===================== TMA producer =====================
+    if (elect_one()) {
+      tma_prefetch_desc(&tq);
+      tma_prefetch_desc(&tk);
+      tma_prefetch_desc(&tv);
+      mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int c = 0; c < C::NCH; ++c)
+          tma_load_4d(sQ + t * C::TILE_BYTES + c * C::CHUNK_BYTES, &tq, q_full, c * C::CH,
+                      qp * 256 + t * 128, ga, gb);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % NST;
+        if (j >= NST) mbar_wait(&kv_empty[s], ((j / NST) - 1) & 1);
+        uint8_t* sk = sKV + s * C::STAGE_BYTES;
+        mbar_arrive_expect_tx(&k_full[s], C::TILE_BYTES);
+#pragma unroll
+        for (int c = 0; c < C::NCH; ++c)
+          tma_load_4d(sk + c * C::CHUNK_BYTES, &tk, &k_full[s], c * C::CH, j * 128, ga, gb);
+        mbar_arrive_expect_tx(&v_full[s], C::TILE_BYTES);
+#pragma unroll
+        for (int c = 0; c < C::NCH; ++c)
+          tma_load_4d(sk + C::TILE_BYTES + c * C::CHUNK_BYTES, &tv, &v_full[s], c * C::CH, j * 128, ga, gb);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 9) {
+    // ===================== MMA issuer =====================
+    if (elect_one()) {
+      constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, 0, 1);
+      constexpr uint32_t swz = (C::SWB == 128) ? SWZ_128B : SWZ_64B;
+      const uint32_t q_addr = smem_u32(sQ);
+      auto issue_s = [&](int t, int j) {
+        const uint32_t ka = smem_u32(sKV + (j % NST) * C::STAGE_BYTES);
+        const uint32_t qa = q_addr + t * C::TILE_BYTES;
+        const uint32_t dS = tmem + (t ? C::COL_S1 : C::COL_S0);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k * 16 / C::CH) * C::CHUNK_BYTES + (k * 16 % C::CH) * 2;
+          mma_ss(dS, make_sdesc(qa + off, 16, 8 * C::SWB, swz), make_sdesc(ka + off, 16, 8 * C::SWB, swz),
+                 idesc_qk, k > 0);
+        }
+        mma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {
+        const uint32_t va = smem_u32(sKV + (j % NST) * C::STAGE_BYTES + C::TILE_BYTES);
+        const uint32_t aP = tmem + (t ? C::COL_S1 : C::COL_S0) + 64;
+        const uint32_t dO = tmem + (t ? C::COL_O1 : C::COL_O0);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          mma_ts(dO, aP + 8 * k, make_sdesc(va + k * 16 * C::SWB, C::CHUNK_BYTES, 8 * C::SWB, swz), idesc_pv,
+                 (j > 0 || k > 0) ? 1u : 0u);
+        mma_commit(&o_full[t]);
+      };
+
+      mbar_wait(q_full, 0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % NST;
+        const uint32_t ph = (j / NST) & 1;
+        mbar_wait(&v_full[s], ph);
+        const bool more = j + 1 < nkv;
+        const int s1 = (j + 1) % NST;
+        const uint32_t ph1 = ((j + 1) / NST) & 1;
+        // tile 0
+        mbar_wait(&p_full[0], j & 1);
+        tc_fence_after();
+        issue_pv(0, j);
+        if (more) {
+          mbar_wait(&k_full[s1], ph1);
+          tc_fence_after();
+          issue_s(0, j + 1);
+        }
+        // tile 1
+        mbar_wait(&p_full[1], j & 1);
+        tc_fence_after();
+        issue_pv(1, j);
+        mma_commit(&kv_empty[s]);  // K_j, V_j no longer read once these MMAs retire
+        if (more) issue_s(1, j + 1);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== softmax warpgroups (warps 0-7) =====================
+    const int t = warp >> 2;                                   // query tile of this warpgroup
+    const uint32_t row = (warp & 3) * 32 + lane;               // tile row == TMEM lane
+    const uint32_t lane_base = ((warp & 3) * 32) << 16;
+    const uint32_t tSrow = tmem + lane_base + (t ? C::COL_S1 : C::COL_S0);
+    const uint32_t tOrow = tmem + lane_base + (t ? C::COL_O1 : C::COL_O0);
+    const float sl2 = p.scale_log2;
+    float m_run = -INFINITY;  // running max, log2-scaled units
+    float l_run = 0.f;
+
+    for (int j = 0; j < nkv; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      uint32_t sv[128];
+#pragma unroll
+      for (int c = 0; c < 128; c += 32) tmem_ld_x32(tSrow + c, sv + c);
+      tmem_wait_ld();
+      const int valid = L - j * 128;  // columns >= valid are beyond the sequence
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        const float v = __uint_as_float(sv[c]);
+        mx = (c < valid) ? fmaxf(mx, v) : mx;
+      }
+      const float m_new = fmaxf(m_run, mx * sl2);
+      if (j == 0) {
+        m_run = m_new;
+      } else {
+        const bool need = (m_new - m_run) > RESCALE_LOG2;
+        if (__any_sync(0xffffffffu, need)) {
+          // Move the max for the whole warp (exact for every row); rescale O_t
+          // once PV_t^{j-1} has retired.
+          const float alpha = ex2(m_run - m_new);
+          l_run *= alpha;
+          m_run = m_new;
+          mbar_wait(&o_full[t], (j - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < D; c += 32) {
+            uint32_t ov[32];
+            tmem_ld_x32(tOrow + c, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+            tmem_st_x32(tOrow + c, ov);
+          }
+        }
+      }
+      const float mb = m_run;
+      float lsum = 0.f;
+      uint32_t pk[64];
+#pragma unroll
+      for (int c = 0; c < 128; c += 2) {
+        const float p0 = (c < valid) ? ex2(fmaf(__uint_as_float(sv[c]), sl2, -mb)) : 0.f;
+        const float p1 = (c + 1 < valid) ? ex2(fmaf(__uint_as_float(sv[c + 1]), sl2, -mb)) : 0.f;
+        lsum += p0 + p1;
+        pk[c / 2] = pack_bf16x2(p0, p1);
+      }
+      l_run += lsum;
+#pragma unroll
+      for (int c = 0; c < 64; c += 32) tmem_st_x32(tSrow + 64 + c, pk + c);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[t]);
+    }
+
+    // ---- epilogue ----
+    mbar_wait(&o_full[t], (nkv - 1) & 1);
+    tc_fence_after();
+    float o[D];
+#pragma unroll
+    for (int c = 0; c < D; c += 32) tmem_ld_x32(tOrow + c, reinterpret_cast<uint32_t*>(o + c));
+    tmem_wait_ld();
+    const int l_idx = qp * 256 + t * 128 + (int)row;
+    if (l_idx < L) {
+      const long long off = (long long)l_idx * p.sL + (long long)ga * p.sA + (long long)gb * p.sB;
+      epilogue_row<D, 128, EPI>(p, o, 1.0f / l_run, off, sQ + t * C::TILE_BYTES, row);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace tsf

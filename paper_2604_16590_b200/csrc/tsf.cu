@@ -1,0 +1,614 @@
+// libtsf.so: C ABI (include/tsf.h) over the sm_100a kernels.
+//
+// Host side only: validation, TMA tensor maps, kernel selection and launch,
+// workspace, NCCL all-to-all for the distributed block, stage timing.
+#include "../../include/tsf.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "attn_flash.cuh"
+#include "attn_packed.cuh"
+#include "layout.cuh"
+
+using namespace tsf;
+
+struct StageRec {
+  int stage;
+  cudaEvent_t e0, e1;
+};
+
+struct tsf_handle {
+  int K = 0, N = 0, H = 0, d = 0;
+  int rank = 0, world = 1;
+  int device = 0, num_sms = 148;
+  ncclComm_t comm = nullptr;
+  // workspace (device)
+  __nv_bfloat16 *hi = nullptr, *lo = nullptr;    // X_t planes, [K, N/P, H, d]
+  __nv_bfloat16 *rhi = nullptr, *rlo = nullptr;  // dist: all-to-all receive [P][K/P][N/P][H][d]
+  __nv_bfloat16 *uhi = nullptr, *ulo = nullptr;  // dist: unpacked frame shard [K/P][N][H][d]
+  __nv_bfloat16* xdev = nullptr;                 // host API staging
+  float* ydev = nullptr;
+  std::string err;
+  int launches = 0;
+  bool timing = false;
+  std::vector<StageRec> recs;
+  std::vector<cudaEvent_t> event_pool;
+};
+
+static thread_local std::string g_create_err;
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+static tsf_status fail(tsf_handle* h, tsf_status s, const std::string& msg) {
+  if (h) h->err = msg;
+  else g_create_err = msg;
+  return s;
+}
+#define TSF_CUDA(h, call)                                                                          \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      return fail(h, TSF_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));          \
+  } while (0)
+#define TSF_NCCL(h, call)                                                                          \
+  do {                                                                                             \
+    ncclResult_t r_ = (call);                                                                      \
+    if (r_ != ncclSuccess)                                                                         \
+      return fail(h, TSF_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));          \
+  } while (0)
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+// A sequence view of a [*, *, H, d] bf16 tensor (see attn_common.cuh).
+struct View {
+  int L, A, B;
+  long long sL, sA, sB;  // element strides
+};
+
+static View temporal_view(int K, int Nl, int H, int d) {  // groups (h, n), axis t
+  return View{K, H, Nl, (long long)Nl * H * d, (long long)d, (long long)H * d};
+}
+static View spatial_view(int Kl, int N, int H, int d) {  // groups (h, t), axis n
+  return View{N, H, Kl, (long long)H * d, (long long)d, (long long)N * H * d};
+}
+
+// 4-D tensor map (d, L, A, B) with box (CH, boxL, boxA, boxB).
+static tsf_status make_map(tsf_handle* h, CUtensorMap* m, const void* base, int d, const View& v, int boxL, int boxA,
+                           int boxB) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return fail(h, TSF_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  const int swb = (2 * d < 128) ? 2 * d : 128;
+  cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)v.L, (cuuint64_t)v.A, (cuuint64_t)v.B};
+  cuuint64_t strides[3] = {(cuuint64_t)v.sL * 2, (cuuint64_t)v.sA * 2, (cuuint64_t)v.sB * 2};
+  cuuint32_t box[4] = {(cuuint32_t)(swb / 2), (cuuint32_t)boxL, (cuuint32_t)boxA, (cuuint32_t)boxB};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d): dims %llu %llu %llu %llu box %u %u %u %u", (int)r,
+             (unsigned long long)dims[0], (unsigned long long)dims[1], (unsigned long long)dims[2],
+             (unsigned long long)dims[3], box[0], box[1], box[2], box[3]);
+    return fail(h, TSF_ERR_CUDA, buf);
+  }
+  return TSF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// stage timing
+// ---------------------------------------------------------------------------
+static cudaEvent_t pool_event(tsf_handle* h) {
+  if (!h->event_pool.empty()) {
+    cudaEvent_t e = h->event_pool.back();
+    h->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+struct StageTimer {
+  tsf_handle* h;
+  cudaStream_t s;
+  int stage;
+  cudaEvent_t e0 = nullptr;
+  StageTimer(tsf_handle* h_, cudaStream_t s_, int st) : h(h_), s(s_), stage(st) {
+    if (h->timing) {
+      e0 = pool_event(h);
+      cudaEventRecord(e0, s);
+    }
+  }
+  void done() {
+    if (e0) {
+      cudaEvent_t e1 = pool_event(h);
+      cudaEventRecord(e1, s);
+      h->recs.push_back({stage, e0, e1});
+      e0 = nullptr;
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// kernel launch
+// ---------------------------------------------------------------------------
+template <typename KernelT>
+static tsf_status launch(tsf_handle* h, KernelT kern, int grid, int threads, int smem, cudaStream_t st,
+                         const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const AttnParams& p) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return fail(h, TSF_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  kern<<<grid, threads, smem, st>>>(mq, mk, mv, p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(h, TSF_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
+  h->launches++;
+  return TSF_OK;
+}
+
+template <int D, int WIN, int EPI, bool SHARED>
+static tsf_status launch_packed_t(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
+                                  const CUtensorMap& mv, const AttnParams& p) {
+  constexpr int NST = SHARED ? 4 : 2;
+  using C = PackedCfg<D, WIN, EPI, SHARED, NST>;
+  const int per_sm = (C::TCOLS == 256 && 2 * C::SMEM <= 227 * 1024) ? 2 : 1;
+  int grid = h->num_sms * per_sm;
+  if (grid > p.num_tiles) grid = p.num_tiles;
+  return launch(h, attn_packed_kernel<D, WIN, EPI, SHARED, NST>, grid, C::THREADS, C::SMEM, st, mq, mk, mv, p);
+}
+
+template <int D, int EPI>
+static tsf_status launch_flash_t(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
+                                 const CUtensorMap& mv, const AttnParams& p) {
+  constexpr int NST = (D == 128) ? 2 : 4;
+  using C = FlashCfg<D, EPI, NST>;
+  const long long grid = (long long)p.n_qpairs * p.A * p.B;
+  if (grid > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "grid too large");
+  return launch(h, attn_flash_kernel<D, EPI, NST>, (int)grid, C::THREADS, C::SMEM, st, mq, mk, mv, p);
+}
+
+template <int D, int EPI, bool SHARED>
+static tsf_status dispatch_packed_win(tsf_handle* h, int win, cudaStream_t st, const CUtensorMap& mq,
+                                      const CUtensorMap& mk, const CUtensorMap& mv, const AttnParams& p) {
+  switch (win) {
+    case 32: return launch_packed_t<D, 32, EPI, SHARED>(h, st, mq, mk, mv, p);
+    case 64: return launch_packed_t<D, 64, EPI, SHARED>(h, st, mq, mk, mv, p);
+    default: return launch_packed_t<D, 128, EPI, SHARED>(h, st, mq, mk, mv, p);
+  }
+}
+
+template <int D>
+static tsf_status dispatch_d(tsf_handle* h, bool packed, int win, int epi, cudaStream_t st, const CUtensorMap& mq,
+                             const CUtensorMap& mk, const CUtensorMap& mv, const AttnParams& p) {
+  if (packed) {
+    switch (epi) {
+      case EPI_BF16: return dispatch_packed_win<D, EPI_BF16, false>(h, win, st, mq, mk, mv, p);
+      case EPI_BLOCK_T: return dispatch_packed_win<D, EPI_BLOCK_T, true>(h, win, st, mq, mk, mv, p);
+      default: return dispatch_packed_win<D, EPI_BLOCK_S, true>(h, win, st, mq, mk, mv, p);
+    }
+  }
+  switch (epi) {
+    case EPI_BF16: return launch_flash_t<D, EPI_BF16>(h, st, mq, mk, mv, p);
+    case EPI_BLOCK_T: return launch_flash_t<D, EPI_BLOCK_T>(h, st, mq, mk, mv, p);
+    default: return launch_flash_t<D, EPI_BLOCK_S>(h, st, mq, mk, mv, p);
+  }
+}
+
+// Attention over one view: q/k/v (q == k == v for the block stages).
+static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, const void* k, const void* vv, int epi,
+                                void* o, void* o2, const void* res_lo, float* y, cudaStream_t st) {
+  const int d = h->d;
+  if ((long long)v.A * v.B == 0 || v.L == 0) return TSF_OK;
+  AttnParams p{};
+  p.L = v.L; p.A = v.A; p.B = v.B;
+  p.sL = v.sL; p.sA = v.sA; p.sB = v.sB;
+  p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
+  p.o = reinterpret_cast<__nv_bfloat16*>(o);
+  p.o2 = reinterpret_cast<__nv_bfloat16*>(o2);
+  p.res_lo = reinterpret_cast<const __nv_bfloat16*>(res_lo);
+  p.y = y;
+  const bool packed = v.L <= 128;
+  int win = 128;
+  CUtensorMap mq, mk, mv;
+  tsf_status s;
+  if (packed) {
+    const int G = 128 / v.L;
+    int Ab = 1;
+    for (int a = 1; a <= G && a <= v.A; ++a)
+      if (v.A % a == 0) Ab = a;
+    int Bb = G / Ab;
+    if (Bb > v.B) Bb = v.B;
+    p.Ab = Ab; p.Bb = Bb;
+    p.tiles_a = v.A / Ab;
+    const long long tiles = (long long)p.tiles_a * ((v.B + Bb - 1) / Bb);
+    if (tiles > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "too many tiles");
+    p.num_tiles = (int)tiles;
+    win = (32 % v.L == 0) ? 32 : (64 % v.L == 0) ? 64 : 128;
+    if ((s = make_map(h, &mq, q, d, v, v.L, Ab, Bb)) != TSF_OK) return s;
+    if ((s = make_map(h, &mk, k, d, v, v.L, Ab, Bb)) != TSF_OK) return s;
+    if ((s = make_map(h, &mv, vv, d, v, v.L, Ab, Bb)) != TSF_OK) return s;
+  } else {
+    p.n_qpairs = (v.L + 255) / 256;
+    p.nkv = (v.L + 127) / 128;
+    if ((s = make_map(h, &mq, q, d, v, 128, 1, 1)) != TSF_OK) return s;
+    if ((s = make_map(h, &mk, k, d, v, 128, 1, 1)) != TSF_OK) return s;
+    if ((s = make_map(h, &mv, vv, d, v, 128, 1, 1)) != TSF_OK) return s;
+  }
+  switch (d) {
+    case 32: return dispatch_d<32>(h, packed, win, epi, st, mq, mk, mv, p);
+    case 64: return dispatch_d<64>(h, packed, win, epi, st, mq, mk, mv, p);
+    default: return dispatch_d<128>(h, packed, win, epi, st, mq, mk, mv, p);
+  }
+}
+
+static int grid_for(tsf_handle* h, long long work_items) {
+  long long g = (work_items + 255) / 256;
+  const long long cap = (long long)h->num_sms * 8;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// ---------------------------------------------------------------------------
+// validation
+// ---------------------------------------------------------------------------
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+static bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+  const char *x = (const char*)a, *y = (const char*)b;
+  return x < y + nb && y < x + na;
+}
+
+static tsf_status check_ptrs(tsf_handle* h, std::initializer_list<const void*> ins, const void* out, size_t in_bytes,
+                             size_t out_bytes) {
+  if (!out || !aligned16(out)) return fail(h, TSF_ERR_CONFIG, "output pointer null or not 16-byte aligned");
+  for (const void* p : ins) {
+    if (!p || !aligned16(p)) return fail(h, TSF_ERR_CONFIG, "input pointer null or not 16-byte aligned");
+    if (overlap(p, in_bytes, out, out_bytes)) return fail(h, TSF_ERR_CONFIG, "output overlaps an input");
+  }
+  return TSF_OK;
+}
+
+static tsf_status check_device(tsf_handle* h, int* dev, int* sms) {
+  TSF_CUDA(h, cudaGetDevice(dev));
+  cudaDeviceProp prop;
+  TSF_CUDA(h, cudaGetDeviceProperties(&prop, *dev));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(h, TSF_ERR_UNSUPPORTED, "device is not sm_100 (B200): compute capability " +
+                                            std::to_string(prop.major) + "." + std::to_string(prop.minor));
+  *sms = prop.multiProcessorCount;
+  return TSF_OK;
+}
+
+static tsf_status check_shape(int K, int N, int H, int d, int world) {
+  if (K < 1 || N < 1 || H < 1) return fail(nullptr, TSF_ERR_CONFIG, "K, N, H must be >= 1");
+  if (d != 32 && d != 64 && d != 128) return fail(nullptr, TSF_ERR_UNSUPPORTED, "d must be 32, 64 or 128");
+  if (world < 1) return fail(nullptr, TSF_ERR_CONFIG, "world must be >= 1");
+  if (K % world || N % world) return fail(nullptr, TSF_ERR_CONFIG, "K and N must be divisible by the world size");
+  if ((long long)K * N * H * d >= (1LL << 40)) return fail(nullptr, TSF_ERR_CONFIG, "tensor too large");
+  return TSF_OK;
+}
+
+static tsf_status alloc_workspace(tsf_handle* h) {
+  const size_t El = (size_t)h->K * (h->N / h->world) * h->H * h->d;  // token-shard elements
+  auto a = [&](__nv_bfloat16** p, size_t n) -> bool {
+    return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(__nv_bfloat16)) == cudaSuccess;
+  };
+  bool ok = a(&h->hi, El) && a(&h->lo, El);
+  if (ok && h->world > 1) ok = a(&h->rhi, El) && a(&h->rlo, El) && a(&h->uhi, El) && a(&h->ulo, El);
+  if (!ok) {
+    cudaGetLastError();
+    return fail(nullptr, TSF_ERR_NOMEM, "workspace cudaMalloc failed");
+  }
+  return TSF_OK;
+}
+
+static void free_workspace(tsf_handle* h) {
+  for (void* p : {(void*)h->hi, (void*)h->lo, (void*)h->rhi, (void*)h->rlo, (void*)h->uhi, (void*)h->ulo,
+                  (void*)h->xdev, (void*)h->ydev})
+    if (p) cudaFree(p);
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+tsf_status tsf_create(int K, int N, int H, int d, tsf_handle** out) {
+  if (!out) return fail(nullptr, TSF_ERR_CONFIG, "out is null");
+  *out = nullptr;
+  tsf_status s = check_shape(K, N, H, d, 1);
+  if (s != TSF_OK) return s;
+  tsf_handle* h = new tsf_handle();
+  h->K = K; h->N = N; h->H = H; h->d = d;
+  if ((s = check_device(nullptr, &h->device, &h->num_sms)) != TSF_OK || (s = alloc_workspace(h)) != TSF_OK) {
+    free_workspace(h);
+    delete h;
+    return s;
+  }
+  *out = h;
+  return TSF_OK;
+}
+
+tsf_status tsf_get_unique_id(void* id128) {
+  if (!id128) return fail(nullptr, TSF_ERR_CONFIG, "id128 is null");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, TSF_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  memcpy(id128, &id, sizeof id);
+  return TSF_OK;
+}
+
+tsf_status tsf_create_dist(int K, int N, int H, int d, const void* id128, int rank, int world, tsf_handle** out) {
+  if (!out || !id128) return fail(nullptr, TSF_ERR_CONFIG, "null argument");
+  *out = nullptr;
+  tsf_status s = check_shape(K, N, H, d, world);
+  if (s != TSF_OK) return s;
+  if (rank < 0 || rank >= world) return fail(nullptr, TSF_ERR_CONFIG, "rank out of range");
+  tsf_handle* h = new tsf_handle();
+  h->K = K; h->N = N; h->H = H; h->d = d;
+  h->rank = rank; h->world = world;
+  if ((s = check_device(nullptr, &h->device, &h->num_sms)) != TSF_OK || (s = alloc_workspace(h)) != TSF_OK) {
+    free_workspace(h);
+    delete h;
+    return s;
+  }
+  if (world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, id128, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&h->comm, world, id, rank);
+    if (r != ncclSuccess) {
+      free_workspace(h);
+      delete h;
+      return fail(nullptr, TSF_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+  }
+  *out = h;
+  return TSF_OK;
+}
+
+void tsf_destroy(tsf_handle* h) {
+  if (!h) return;
+  if (h->comm) {
+    ncclResult_t async_err = ncclSuccess;
+    ncclCommGetAsyncError(h->comm, &async_err);
+    if (async_err != ncclSuccess) ncclCommAbort(h->comm);
+    else ncclCommDestroy(h->comm);
+  }
+  for (auto& r : h->recs) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); }
+  for (auto e : h->event_pool) cudaEventDestroy(e);
+  free_workspace(h);
+  delete h;
+}
+
+const char* tsf_last_error(const tsf_handle* h) { return h ? h->err.c_str() : g_create_err.c_str(); }
+
+int tsf_last_launch_count(const tsf_handle* h) { return h ? h->launches : 0; }
+
+tsf_status tsf_set_timing(tsf_handle* h, int enable) {
+  if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
+  for (auto& r : h->recs) { h->event_pool.push_back(r.e0); h->event_pool.push_back(r.e1); }
+  h->recs.clear();
+  h->timing = enable != 0;
+  return TSF_OK;
+}
+
+tsf_status tsf_stage_ms(tsf_handle* h, int stage, float* total_ms, int* n_records) {
+  if (!h || !total_ms) return fail(h, TSF_ERR_CONFIG, "null argument");
+  float tot = 0.f;
+  int n = 0;
+  for (auto& r : h->recs) {
+    if (r.stage != stage) continue;
+    TSF_CUDA(h, cudaEventSynchronize(r.e1));
+    float ms = 0.f;
+    TSF_CUDA(h, cudaEventElapsedTime(&ms, r.e0, r.e1));
+    tot += ms;
+    ++n;
+  }
+  *total_ms = tot;
+  if (n_records) *n_records = n;
+  return TSF_OK;
+}
+
+tsf_status tsf_temporal_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v, tsf_bf16* o,
+                             void* stream) {
+  if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
+  h->launches = 0;
+  const int Nl = h->N / h->world;
+  const size_t bytes = (size_t)h->K * Nl * h->H * h->d * 2;
+  tsf_status s = check_ptrs(h, {q, k, v}, o, bytes, bytes);
+  if (s != TSF_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  StageTimer tm(h, st, 0);
+  s = run_attention(h, temporal_view(h->K, Nl, h->H, h->d), q, k, v, EPI_BF16, o, nullptr, nullptr, nullptr, st);
+  tm.done();
+  return s;
+}
+
+tsf_status tsf_spatial_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v, tsf_bf16* o,
+                            void* stream) {
+  if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
+  h->launches = 0;
+  const int Kl = h->K / h->world;
+  const size_t bytes = (size_t)Kl * h->N * h->H * h->d * 2;
+  tsf_status s = check_ptrs(h, {q, k, v}, o, bytes, bytes);
+  if (s != TSF_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  StageTimer tm(h, st, 1);
+  s = run_attention(h, spatial_view(Kl, h->N, h->H, h->d), q, k, v, EPI_BF16, o, nullptr, nullptr, nullptr, st);
+  tm.done();
+  return s;
+}
+
+// X_t token-sharded planes (hi, lo) -> frame-sharded planes, via one grouped
+// NCCL send/recv round (bytes, bit-exact) and the unpack kernel.
+static tsf_status all_to_all_xt(tsf_handle* h, cudaStream_t st) {
+  const int P = h->world, Kc = h->K / P, Nc = h->N / P;
+  const size_t chunk = (size_t)Kc * Nc * h->H * h->d * 2;  // bytes per peer per plane
+  TSF_NCCL(h, ncclGroupStart());
+  for (int p = 0; p < P; ++p) {
+    TSF_NCCL(h, ncclSend((const char*)h->hi + p * chunk, chunk, ncclUint8, p, h->comm, st));
+    TSF_NCCL(h, ncclSend((const char*)h->lo + p * chunk, chunk, ncclUint8, p, h->comm, st));
+    TSF_NCCL(h, ncclRecv((char*)h->rhi + p * chunk, chunk, ncclUint8, p, h->comm, st));
+    TSF_NCCL(h, ncclRecv((char*)h->rlo + p * chunk, chunk, ncclUint8, p, h->comm, st));
+  }
+  TSF_NCCL(h, ncclGroupEnd());
+  const int vecs = h->H * h->d * 2 / 16;
+  const long long items = (long long)P * Kc * Nc * vecs;
+  reshard_perm_kernel<true><<<grid_for(h, items), 256, 0, st>>>((const uint4*)h->rhi, (uint4*)h->uhi,
+                                                                (const uint4*)h->rlo, (uint4*)h->ulo, P, Kc, Nc, vecs);
+  TSF_CUDA(h, cudaGetLastError());
+  h->launches++;
+  return TSF_OK;
+}
+
+tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void* stream) {
+  if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
+  h->launches = 0;
+  const int P = h->world, Nl = h->N / P, Kl = h->K / P;
+  const size_t in_bytes = (size_t)h->K * Nl * h->H * h->d * 2;
+  const size_t out_bytes = (size_t)Kl * h->N * h->H * h->d * 4;
+  tsf_status s = check_ptrs(h, {x}, y, in_bytes, out_bytes);
+  if (s != TSF_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  // temporal stage: X_t = x + T(x, x, x) -> (hi, lo)
+  {
+    StageTimer tm(h, st, 0);
+    s = run_attention(h, temporal_view(h->K, Nl, h->H, h->d), x, x, x, EPI_BLOCK_T, h->hi, h->lo, nullptr, nullptr,
+                      st);
+    tm.done();
+    if (s != TSF_OK) return s;
+  }
+  const __nv_bfloat16 *shi = h->hi, *slo = h->lo;
+  if (P > 1) {
+    StageTimer tm(h, st, 2);
+    s = all_to_all_xt(h, st);
+    tm.done();
+    if (s != TSF_OK) return s;
+    shi = h->uhi;
+    slo = h->ulo;
+  }
+  // spatial stage: y = X_t + S(hi, hi, hi), residual hi + lo
+  StageTimer tm(h, st, 1);
+  s = run_attention(h, spatial_view(Kl, h->N, h->H, h->d), shi, shi, shi, EPI_BLOCK_S, nullptr, nullptr, slo, y, st);
+  tm.done();
+  return s;
+}
+
+tsf_status tsf_spacetime_block_host(tsf_handle* h, const tsf_bf16* x_host, float* y_host, void* stream) {
+  if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
+  if (!x_host || !y_host) return fail(h, TSF_ERR_CONFIG, "null host buffer");
+  const int P = h->world, Nl = h->N / P, Kl = h->K / P;
+  const size_t in_bytes = (size_t)h->K * Nl * h->H * h->d * 2;
+  const size_t out_bytes = (size_t)Kl * h->N * h->H * h->d * 4;
+  if (!h->xdev) {
+    if (cudaMalloc(&h->xdev, in_bytes) != cudaSuccess || cudaMalloc(&h->ydev, out_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(h, TSF_ERR_NOMEM, "staging cudaMalloc failed");
+    }
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  {
+    StageTimer tm(h, st, 3);
+    TSF_CUDA(h, cudaMemcpyAsync(h->xdev, x_host, in_bytes, cudaMemcpyHostToDevice, st));
+    tm.done();
+  }
+  tsf_status s = tsf_spacetime_block(h, reinterpret_cast<const tsf_bf16*>(h->xdev), h->ydev, stream);
+  if (s != TSF_OK) return s;
+  {
+    StageTimer tm(h, st, 3);
+    TSF_CUDA(h, cudaMemcpyAsync(y_host, h->ydev, out_bytes, cudaMemcpyDeviceToHost, st));
+    tm.done();
+  }
+  TSF_CUDA(h, cudaStreamSynchronize(st));
+  return TSF_OK;
+}
+
+tsf_status tsf_reshard(tsf_handle* h, int dir, const tsf_bf16* in, tsf_bf16* out, void* stream) {
+  if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
+  if (dir != TSF_T2S && dir != TSF_S2T) return fail(h, TSF_ERR_CONFIG, "bad direction");
+  h->launches = 0;
+  const int P = h->world, Kc = h->K / P, Nc = h->N / P;
+  const size_t bytes = (size_t)h->K * Nc * h->H * h->d * 2;  // same size both ways
+  tsf_status s = check_ptrs(h, {in}, out, bytes, bytes);
+  if (s != TSF_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  StageTimer tm(h, st, 2);
+  if (P == 1) {
+    TSF_CUDA(h, cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, st));
+    tm.done();
+    return TSF_OK;
+  }
+  const size_t chunk = bytes / P;
+  const int vecs = h->H * h->d * 2 / 16;
+  const long long items = (long long)P * Kc * Nc * vecs;
+  if (dir == TSF_T2S) {
+    // send frames [p Kc, (p+1) Kc) of the token shard (contiguous); receive
+    // [P][Kc][Nc] blocks, unpack to [Kc][N]
+    TSF_NCCL(h, ncclGroupStart());
+    for (int p = 0; p < P; ++p) {
+      TSF_NCCL(h, ncclSend((const char*)in + p * chunk, chunk, ncclUint8, p, h->comm, st));
+      TSF_NCCL(h, ncclRecv((char*)h->rhi + p * chunk, chunk, ncclUint8, p, h->comm, st));
+    }
+    TSF_NCCL(h, ncclGroupEnd());
+    reshard_perm_kernel<true><<<grid_for(h, items), 256, 0, st>>>((const uint4*)h->rhi, (uint4*)out, nullptr,
+                                                                  nullptr, P, Kc, Nc, vecs);
+  } else {
+    // pack [Kc][N] -> [P][Kc][Nc], send block p to peer p; the received
+    // blocks [P][Kc][Nc] are exactly the token shard [K][Nc]
+    reshard_perm_kernel<false><<<grid_for(h, items), 256, 0, st>>>((const uint4*)in, (uint4*)h->rhi, nullptr,
+                                                                   nullptr, P, Kc, Nc, vecs);
+    TSF_CUDA(h, cudaGetLastError());
+    TSF_NCCL(h, ncclGroupStart());
+    for (int p = 0; p < P; ++p) {
+      TSF_NCCL(h, ncclSend((const char*)h->rhi + p * chunk, chunk, ncclUint8, p, h->comm, st));
+      TSF_NCCL(h, ncclRecv((char*)out + p * chunk, chunk, ncclUint8, p, h->comm, st));
+    }
+    TSF_NCCL(h, ncclGroupEnd());
+  }
+  TSF_CUDA(h, cudaGetLastError());
+  h->launches++;
+  tm.done();
+  return TSF_OK;
+}
+
+tsf_status tsf_transpose(tsf_handle* h, int A, int B, const tsf_bf16* in, tsf_bf16* out, void* stream) {
+  if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
+  if (A < 1 || B < 1) return fail(h, TSF_ERR_CONFIG, "A, B must be >= 1");
+  h->launches = 0;
+  const size_t bytes = (size_t)A * B * h->H * h->d * 2;
+  tsf_status s = check_ptrs(h, {in}, out, bytes, bytes);
+  if (s != TSF_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int vecs = h->H * h->d * 2 / 16;
+  StageTimer tm(h, st, 4);
+  transpose_rows_kernel<<<grid_for(h, (long long)A * B * vecs), 256, 0, st>>>((const uint4*)in, (uint4*)out, nullptr,
+                                                                               nullptr, A, B, vecs);
+  TSF_CUDA(h, cudaGetLastError());
+  tm.done();
+  h->launches++;
+  return TSF_OK;
+}
+
+}  // extern "C"

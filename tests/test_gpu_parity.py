@@ -1,0 +1,199 @@
+"""Parity of the CUDA path (libtsf.so via the C ABI) with the fp64 oracle.
+
+Bar (BASELINE.json north_star): max-abs error <= 2e-2 and relative L2 error
+<= 1e-2 against the oracle evaluated on the same bf16 inputs.  Sizes span
+several 128-row tiles with ragged tails; the full BASELINE sizes are checked on
+sampled rows and full (t, h) planes the oracle computes one by one.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS, REL_L2 = 2e-2, 1e-2
+
+
+def to_dev(bits):
+    return synth.bits_to_torch(bits, "cuda")
+
+
+def f64(bits):
+    return synth.bf16_bits_to_f64(bits)
+
+
+def check(got, want, what):
+    got = np.asarray(got, dtype=np.float64)
+    err = np.abs(got - want)
+    rel = np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30)
+    assert np.all(np.isfinite(got)), f"{what}: non-finite output"
+    assert err.max() <= MAX_ABS and rel <= REL_L2, \
+        f"{what}: max-abs {err.max():.3e} rel-L2 {rel:.3e} (max|ref| {np.abs(want).max():.2f})"
+    return err.max(), rel
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.double().cpu().numpy()
+
+
+# shapes: (K, N, H, d) -- cover packed (L <= 128) and flash (L > 128) paths,
+# all three head dims, ragged tails, degenerate K = 1 / N = 1
+ATTN_SHAPES = [
+    (4, 64, 2, 32),      # C1
+    (8, 300, 2, 64),     # spatial flash: 3 KV tiles, ragged; temporal packed K=8
+    (12, 130, 3, 64),    # temporal packed K=12 (G=10, WIN=128); spatial 2 KV tiles, tail of 2
+    (5, 256, 2, 128),    # d=128; temporal K=5
+    (200, 4, 2, 64),     # temporal flash K=200 (ragged); spatial packed N=4
+    (1, 513, 1, 64),     # K=1: temporal = v exactly; spatial 5 KV tiles
+    (33, 1, 3, 32),      # N=1: spatial = v exactly
+    (128, 40, 2, 64),    # temporal packed with L=128 (G=1)
+    (2, 100, 4, 32),     # spatial packed N=100 (WIN=128)
+]
+
+
+@pytest.mark.parametrize("shape", ATTN_SHAPES)
+@pytest.mark.parametrize("kind", ["field", "iid"])
+def test_temporal_and_spatial_match_oracle(tsf_lib, shape, kind):
+    K, N, H, d = shape
+    qb, kb, vb = synth.make_qkv(K, N, H, d, seed=3, kind=kind)
+    layer = tsf_lib.Layer(K, N, H, d)
+    q, k, v = to_dev(qb), to_dev(kb), to_dev(vb)
+    ot = host(layer.temporal(q, k, v))
+    os_ = host(layer.spatial(q, k, v))
+    check(ot, oracle.temporal(f64(qb), f64(kb), f64(vb)), f"temporal {shape} {kind}")
+    check(os_, oracle.spatial(f64(qb), f64(kb), f64(vb)), f"spatial {shape} {kind}")
+
+
+@pytest.mark.parametrize("shape", [(4, 64, 2, 32), (6, 260, 2, 64), (1, 200, 2, 128), (130, 3, 1, 64)])
+def test_peaky_softmax(tsf_lib, shape):
+    """q x 4: large logits exercise the online-softmax rescale path."""
+    K, N, H, d = shape
+    qb, kb, vb = synth.make_qkv(K, N, H, d, seed=4, kind="iid", peaky=True)
+    layer = tsf_lib.Layer(K, N, H, d)
+    q, k, v = to_dev(qb), to_dev(kb), to_dev(vb)
+    check(host(layer.spatial(q, k, v)), oracle.spatial(f64(qb), f64(kb), f64(vb)), f"spatial peaky {shape}")
+    check(host(layer.temporal(q, k, v)), oracle.temporal(f64(qb), f64(kb), f64(vb)), f"temporal peaky {shape}")
+
+
+def test_degenerate_reductions_exact(tsf_lib):
+    """K=1 temporal returns v exactly; N=1 spatial returns v exactly (I2/I3)."""
+    qb, kb, vb = synth.make_qkv(1, 96, 2, 64, seed=5)
+    layer = tsf_lib.Layer(1, 96, 2, 64)
+    out = layer.temporal(to_dev(qb), to_dev(kb), to_dev(vb))
+    torch.cuda.synchronize()
+    assert torch.equal(out.cpu(), synth.bits_to_torch(vb))
+    qb, kb, vb = synth.make_qkv(7, 1, 2, 64, seed=5)
+    layer = tsf_lib.Layer(7, 1, 2, 64)
+    out = layer.spatial(to_dev(qb), to_dev(kb), to_dev(vb))
+    torch.cuda.synchronize()
+    assert torch.equal(out.cpu(), synth.bits_to_torch(vb))
+
+
+BLOCK_SHAPES = [(4, 64, 2, 32), (8, 300, 2, 64), (12, 130, 3, 64), (5, 256, 2, 128), (200, 4, 2, 64),
+                (1, 129, 2, 64), (9, 1, 2, 32)]
+
+
+@pytest.mark.parametrize("shape", BLOCK_SHAPES)
+def test_block_matches_oracle(tsf_lib, shape):
+    K, N, H, d = shape
+    xb = synth.make_x(K, N, H, d, seed=6)
+    layer = tsf_lib.Layer(K, N, H, d)
+    y = host(layer.block(to_dev(xb)))
+    check(y, oracle.block(f64(xb)), f"block {shape}")
+
+
+def test_block_is_bitwise_deterministic(tsf_lib):
+    K, N, H, d = 8, 300, 2, 64
+    x = to_dev(synth.make_x(K, N, H, d, seed=7))
+    layer = tsf_lib.Layer(K, N, H, d)
+    a = layer.block(x).clone()
+    b = layer.block(x)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
+def sample_rows(K, N, H, n, seed):
+    g = np.random.default_rng(seed)
+    rows = {(int(g.integers(K)), int(g.integers(N)), int(g.integers(H))) for _ in range(n)}
+    rows |= {(0, 0, 0), (K - 1, N - 1, H - 1), (K - 1, 0, 0), (0, N - 1, H - 1)}
+    return sorted(rows)
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C5"])
+def test_full_size_block_sampled(tsf_lib, cfg):
+    """BASELINE sizes, bench launch configuration, sampled rows + full planes."""
+    w = synth.CONFIGS[cfg]
+    xb = synth.make_x(w.K, w.N, w.H, w.d, seed=0)
+    layer = tsf_lib.Layer(w.K, w.N, w.H, w.d)
+    y = layer.block(to_dev(xb))
+    torch.cuda.synchronize()
+    x = f64(xb)
+    rows = sample_rows(w.K, w.N, w.H, 2048, seed=11)
+    want = oracle.block_rows(x, rows)
+    yi = torch.tensor(rows, dtype=torch.long)
+    got = y[yi[:, 0], yi[:, 1], yi[:, 2]].double().cpu().numpy()
+    check(got, want, f"{cfg} block sampled rows")
+    for t, h in [(0, 0), (w.K - 1, w.H - 1)]:
+        check(y[t, :, h].double().cpu().numpy(), oracle.block_plane(x, t, h), f"{cfg} block plane ({t},{h})")
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C5"])
+def test_full_size_attention_sampled(tsf_lib, cfg):
+    w = synth.CONFIGS[cfg]
+    qb, kb, vb = synth.make_qkv(w.K, w.N, w.H, w.d, seed=1)
+    layer = tsf_lib.Layer(w.K, w.N, w.H, w.d)
+    q, k, v = to_dev(qb), to_dev(kb), to_dev(vb)
+    ot, os_ = layer.temporal(q, k, v), layer.spatial(q, k, v)
+    torch.cuda.synchronize()
+    rows = sample_rows(w.K, w.N, w.H, 2048, seed=12)
+    ri = torch.tensor(rows, dtype=torch.long)
+    qf, kf, vf = f64(qb), f64(kb), f64(vb)
+    check(ot[ri[:, 0], ri[:, 1], ri[:, 2]].double().cpu().numpy(), oracle.temporal_rows(qf, kf, vf, rows),
+          f"{cfg} temporal sampled")
+    check(os_[ri[:, 0], ri[:, 1], ri[:, 2]].double().cpu().numpy(), oracle.spatial_rows(qf, kf, vf, rows),
+          f"{cfg} spatial sampled")
+
+
+def test_block_host_api_matches_device_api(tsf_lib):
+    K, N, H, d = 8, 300, 2, 64
+    xb = synth.make_x(K, N, H, d, seed=8)
+    layer = tsf_lib.Layer(K, N, H, d)
+    y_dev = layer.block(to_dev(xb))
+    xh = synth.bits_to_torch(xb).pin_memory()
+    yh = torch.empty((K, N, H, d), dtype=torch.float32).pin_memory()
+    layer.block_host(xh, yh)
+    torch.cuda.synchronize()
+    assert torch.equal(y_dev.cpu(), yh)
+
+
+def test_transpose_is_exact_permutation(tsf_lib):
+    K, N, H, d = 6, 130, 2, 64
+    xb = synth.make_x(K, N, H, d, seed=9)
+    layer = tsf_lib.Layer(K, N, H, d)
+    x = to_dev(xb)
+    t = layer.transpose(x)
+    back = layer.transpose(t)
+    torch.cuda.synchronize()
+    assert torch.equal(t.cpu(), x.cpu().transpose(0, 1).contiguous())
+    assert torch.equal(back, x)
+
+
+def test_abi_errors(tsf_lib):
+    with pytest.raises(tsf_lib.TsfError) as e:
+        tsf_lib.Layer(4, 64, 2, 48)
+    assert e.value.status == tsf_lib.TSF_ERR_UNSUPPORTED
+    with pytest.raises(tsf_lib.TsfError) as e:
+        tsf_lib.Layer(0, 64, 2, 64)
+    assert e.value.status == tsf_lib.TSF_ERR_CONFIG
+    layer = tsf_lib.Layer(4, 64, 2, 32)
+    x = torch.zeros((4, 64, 2, 32), dtype=torch.bfloat16, device="cuda")
+    L = tsf_lib.lib()
+    s = L.tsf_temporal_attn(layer._h, x.data_ptr(), x.data_ptr(), x.data_ptr(), x.data_ptr(), None)
+    assert s == tsf_lib.TSF_ERR_CONFIG                     # output aliases input
+    s = L.tsf_temporal_attn(layer._h, x.data_ptr() + 2, x.data_ptr(), x.data_ptr(), None, None)
+    assert s == tsf_lib.TSF_ERR_CONFIG                     # null / misaligned
+    assert b"aligned" in L.tsf_last_error(layer._h)
