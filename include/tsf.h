@@ -57,7 +57,7 @@ enum { TSF_T2S = 0, TSF_S2T = 1 }; /* reshard directions */
 
 /* Create a single-GPU handle for a [K, N, H, d] layer on the current CUDA
  * device.  K, N, H >= 1; d in {32, 64, 128}.  Allocates the block workspace
- * (X_t as two bf16 planes, 4*K*N*H*d bytes). */
+ * (X_t in fp16, 2*K*N*H*d bytes). */
 tsf_status tsf_create(int K, int N, int H, int d, tsf_handle** out);
 
 /* Temporal attention ("at each spatial location"): for every (n, h),
@@ -76,8 +76,9 @@ tsf_status tsf_spatial_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k,
 /* Divided space-time block, temporal then spatial ("followed by"), with
  * identity projections and residual weight 1 (readings G1, G5):
  *   X_t = x + T(x, x, x);   y = X_t + S(X_t, X_t, X_t).
- * x: bf16.  y: fp32.  X_t is kept as bf16 hi + bf16 lo (X_t = hi + lo to
- * ~2^-17 relative); the MMAs read hi, the residual adds hi + lo (reading G8).
+ * x: bf16.  y: fp32.  X_t is kept in fp16 (11-bit mantissa, reading G8): the
+ * spatial stage's MMAs read it (with fp16 P) and the residual adds it.
+ * Precondition: |X_t| < 65504 (fp16 range), e.g. |x| < 32752.
  * Single GPU: x, y are [K, N, H, d].  Distributed: x is the token shard
  * [K, N/P, H, d], y the frame shard [K/P, N, H, d]; one all-to-all (NCCL,
  * bytes, bit-exact) reshards X_t between the stages. */
@@ -130,7 +131,7 @@ int tsf_last_launch_count(const tsf_handle* h);
  * records), 0 stops.  tsf_stage_ms synchronises on the recorded events and
  * returns the summed milliseconds and the number of recorded launches of
  * stage 0 = temporal attention, 1 = spatial attention, 2 = reshard
- * (all-to-all + unpack), 3 = host<->device copies. */
+ * (all-to-all + unpack), 3 = host<->device copies, 4 = tsf_transpose. */
 tsf_status tsf_set_timing(tsf_handle* h, int enable);
 tsf_status tsf_stage_ms(tsf_handle* h, int stage, float* total_ms, int* n_records);
 

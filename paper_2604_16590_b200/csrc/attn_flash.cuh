@@ -9,12 +9,18 @@
 // S_t = Q_t K_j^T and O_t += P_t V_j between the two tiles so the tensor core
 // works on one tile while the softmax warpgroup of the other runs.
 //
-// TMEM (512 columns): S0 [0,128), S1 [128,256), O0 [256,256+D), O1 after it.
-// P_t (bf16 pairs, 64 columns) overwrites the upper half of S_t after S_t has
-// been read into registers.  Online softmax in the log2 domain with
-// conditional rescaling: the running max is only moved (and O_t rescaled in
-// TMEM) when a row max grows by more than RESCALE_LOG2; the final O/l is exact
-// either way because l is accumulated against the same stale max.
+// TMEM (512 columns): S0 [0,128), S1 [128,256), O0 [256, 256+OW), O1 after
+// it, OW = D (+16 for the l columns when D <= 64).  P_t (16-bit pairs, 64
+// columns) overwrites the upper half of S_t after S_t has been read into
+// registers.  Online softmax in the log2 domain with conditional rescaling:
+// the running max only moves (and O_t is rescaled in TMEM) when a row max
+// grows by more than RESCALE_LOG2; O/l is exact either way because l is
+// accumulated against the same stale max.
+//
+// Softmax denominator: for D <= 64 the MMA warp also multiplies P_t by a
+// column of ones (an N=16 MMA into the l columns after O_t), so l is the exact
+// fp32 sum of the rounded P and the softmax warps spend no ALU on it; for
+// D = 128 (TMEM full) the warps sum the rounded P themselves.
 //
 // Warp roles (320 threads): warps 0-3 softmax of tile 0, warps 4-7 softmax of
 // tile 1 (thread owns TMEM lane = tile row), warp 8 TMA producer, warp 9 MMA
@@ -33,12 +39,16 @@ struct FlashCfg {
   static constexpr int CH = SWB / 2;
   static constexpr int NCH = D / CH;
   static constexpr int CHUNK_BYTES = 128 * SWB;
-  static constexpr int TILE_BYTES = NCH * CHUNK_BYTES;  // 128 x D bf16
+  static constexpr int TILE_BYTES = NCH * CHUNK_BYTES;  // 128 x D 16-bit
   static constexpr int Q_BYTES = 2 * TILE_BYTES;
   static constexpr int STAGE_BYTES = 2 * TILE_BYTES;    // K + V
-  static constexpr int SMEM = Q_BYTES + NST * STAGE_BYTES + 1024 + 256;
+  static constexpr bool ONES = (D <= 64);               // l via an MMA against a ones column
+  static constexpr int ONES_BYTES = 1024;
+  static constexpr int SMEM = Q_BYTES + NST * STAGE_BYTES + ONES_BYTES + 1024 + 256;
   static constexpr int THREADS = 320;
-  static constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 256 + D;
+  static constexpr uint32_t OW = ONES ? D + 16 : D;
+  static constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 256 + OW;
+  static_assert(COL_O1 + OW <= 512, "TMEM budget");
 };
 
 template <int D, int EPI, int NST>
@@ -46,11 +56,13 @@ __global__ void __launch_bounds__(320, 1)
 attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                   const __grid_constant__ CUtensorMap tv, const AttnParams p) {
   using C = FlashCfg<D, EPI, NST>;
+  constexpr bool F16 = EpiTraits<EPI>::F16;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                        // Q0 | Q1
   uint8_t* sKV = smem + C::Q_BYTES;          // NST x (K | V)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + NST * C::STAGE_BYTES);
+  uint8_t* sOnes = sKV + NST * C::STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;               // [NST]
   uint64_t* v_full = k_full + NST;           // [NST]
@@ -66,6 +78,12 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
   const int grp = blockIdx.x / p.n_qpairs;
   const int ga = grp % p.A, gb = grp / p.A;
 
+  if constexpr (C::ONES) {
+    const uint32_t one2 = F16 ? 0x3C003C00u : 0x3F803F80u;
+    for (uint32_t i = threadIdx.x; i < C::ONES_BYTES / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(sOnes)[i] = make_uint4(one2, one2, one2, one2);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     for (int s = 0; s < NST; ++s) {
@@ -117,10 +135,12 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
   } else if (warp == 9) {
     // ===================== MMA issuer =====================
     if (elect_one()) {
-      constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0);
-      constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, 0, 1);
+      constexpr uint32_t idesc_qk = make_idesc(128, 128, 0, 0, F16);
+      constexpr uint32_t idesc_pv = make_idesc(128, D, 0, 1, F16);
+      constexpr uint32_t idesc_l = make_idesc(128, 16, 0, 1, F16);
       constexpr uint32_t swz = (C::SWB == 128) ? SWZ_128B : SWZ_64B;
       const uint32_t q_addr = smem_u32(sQ);
+      const uint64_t ones_desc = make_sdesc(smem_u32(sOnes), 128, 128, SWZ_NONE);
       auto issue_s = [&](int t, int j) {
         const uint32_t ka = smem_u32(sKV + (j % NST) * C::STAGE_BYTES);
         const uint32_t qa = q_addr + t * C::TILE_BYTES;
@@ -138,9 +158,11 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         const uint32_t aP = tmem + (t ? C::COL_S1 : C::COL_S0) + 64;
         const uint32_t dO = tmem + (t ? C::COL_O1 : C::COL_O0);
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          mma_ts(dO, aP + 8 * k, make_sdesc(va + k * 16 * C::SWB, C::CHUNK_BYTES, 8 * C::SWB, swz), idesc_pv,
-                 (j > 0 || k > 0) ? 1u : 0u);
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
+          mma_ts(dO, aP + 8 * k, make_sdesc(va + k * 16 * C::SWB, C::CHUNK_BYTES, 8 * C::SWB, swz), idesc_pv, acc);
+          if constexpr (C::ONES) mma_ts(dO + D, aP + 8 * k, ones_desc, idesc_l, acc);
+        }
         mma_commit(&o_full[t]);
       };
 
@@ -183,7 +205,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     const uint32_t tOrow = tmem + lane_base + (t ? C::COL_O1 : C::COL_O0);
     const float sl2 = p.scale_log2;
     float m_run = -INFINITY;  // running max, log2-scaled units
-    float l_run = 0.f;
+    float l_run = 0.f;        // used when !ONES
 
     for (int j = 0; j < nkv; ++j) {
       mbar_wait(&s_full[t], j & 1);
@@ -206,7 +228,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         const bool need = (m_new - m_run) > RESCALE_LOG2;
         if (__any_sync(0xffffffffu, need)) {
           // Move the max for the whole warp (exact for every row); rescale O_t
-          // once PV_t^{j-1} has retired.
+          // (and its l columns) once PV_t^{j-1} has retired.
           const float alpha = ex2(m_run - m_new);
           l_run *= alpha;
           m_run = m_new;
@@ -221,6 +243,14 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
             for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
             tmem_st_x32(tOrow + c, ov);
           }
+          if constexpr (C::ONES) {
+            uint32_t lv[8];
+            tmem_ld_x8(tOrow + D, lv);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) lv[i] = __float_as_uint(__uint_as_float(lv[i]) * alpha);
+            tmem_st_x8(tOrow + D, lv);
+          }
         }
       }
       const float mb = m_run;
@@ -230,8 +260,11 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       for (int c = 0; c < 128; c += 2) {
         const float p0 = (c < valid) ? ex2(fmaf(__uint_as_float(sv[c]), sl2, -mb)) : 0.f;
         const float p1 = (c + 1 < valid) ? ex2(fmaf(__uint_as_float(sv[c + 1]), sl2, -mb)) : 0.f;
-        lsum += p0 + p1;
-        pk[c / 2] = pack_bf16x2(p0, p1);
+        pk[c / 2] = pack2<F16>(p0, p1);
+        if constexpr (!C::ONES) {
+          const float2 pr = unpack2<F16>(pk[c / 2]);
+          lsum += pr.x + pr.y;
+        }
       }
       l_run += lsum;
 #pragma unroll
@@ -248,7 +281,14 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     float o[D];
 #pragma unroll
     for (int c = 0; c < D; c += 32) tmem_ld_x32(tOrow + c, reinterpret_cast<uint32_t*>(o + c));
-    tmem_wait_ld();
+    if constexpr (C::ONES) {
+      uint32_t lv[8];
+      tmem_ld_x8(tOrow + D, lv);
+      tmem_wait_ld();
+      l_run = __uint_as_float(lv[0]);
+    } else {
+      tmem_wait_ld();
+    }
     const int l_idx = qp * 256 + t * 128 + (int)row;
     if (l_idx < L) {
       const long long off = (long long)l_idx * p.sL + (long long)ga * p.sA + (long long)gb * p.sB;

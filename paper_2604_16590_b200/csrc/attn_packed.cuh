@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(192, (192 + D <= 256) ? 2 : 1)
 attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                    const __grid_constant__ CUtensorMap tv, const AttnParams p) {
   using C = PackedCfg<D, WIN, EPI, SHARED, NST>;
+  constexpr bool F16 = EpiTraits<EPI>::F16;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * C::STAGE_BYTES);
@@ -108,8 +109,8 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
   } else if (warp == 5) {
     // ===================== MMA issuer =====================
     if (elect_one()) {
-      constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0);
-      constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, 0, 1);
+      constexpr uint32_t idesc_qk = make_idesc(128, 128, 0, 0, F16);
+      constexpr uint32_t idesc_pv = make_idesc(128, D, 0, 1, F16);
       for (int i = 0; i < my_tiles; ++i) {
         const int s = i % NST;
         mbar_wait(&full[s], (i / NST) & 1);
@@ -175,6 +176,7 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
         m = ok ? fmaxf(m, __uint_as_float(sv[c])) : m;
       }
       const float mb = (m == -INFINITY) ? 0.f : m * sl2;
+      // l sums the rounded P the PV MMA consumes (weights sum to one exactly)
       float l = 0.f;
       uint32_t pk[WIN / 2];
 #pragma unroll
@@ -183,8 +185,9 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
         const bool ok1 = row_ok && c + 1 >= lo && c + 1 < hi;
         const float p0 = ok0 ? ex2(fmaf(__uint_as_float(sv[c]), sl2, -mb)) : 0.f;
         const float p1 = ok1 ? ex2(fmaf(__uint_as_float(sv[c + 1]), sl2, -mb)) : 0.f;
-        l += p0 + p1;
-        pk[c / 2] = pack_bf16x2(p0, p1);
+        pk[c / 2] = pack2<F16>(p0, p1);
+        const float2 pr = unpack2<F16>(pk[c / 2]);
+        l += pr.x + pr.y;
       }
 #pragma unroll
       for (int c = 0; c < WIN / 2; c += 16) tmem_st_x16(tP + lane_base + colstart / 2 + c, pk + c);

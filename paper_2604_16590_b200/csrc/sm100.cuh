@@ -132,11 +132,13 @@ TSF_DEV void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// Instruction descriptor, kind::f16: bf16 A/B, fp32 D, M x N, majors (0 = K-major, 1 = MN-major).
-__host__ __device__ constexpr uint32_t make_idesc_bf16(uint32_t M, uint32_t N, uint32_t a_major, uint32_t b_major) {
-  return (1u << 4)            // D format F32
-         | (1u << 7)          // A format BF16
-         | (1u << 10)         // B format BF16
+// Instruction descriptor, kind::f16: A/B both bf16 (f16 = false) or both fp16
+// (f16 = true), fp32 D, M x N, majors (0 = K-major, 1 = MN-major).
+__host__ __device__ constexpr uint32_t make_idesc(uint32_t M, uint32_t N, uint32_t a_major, uint32_t b_major,
+                                                  bool f16) {
+  return (1u << 4)                          // D format F32
+         | ((f16 ? 0u : 1u) << 7)           // A format F16 / BF16
+         | ((f16 ? 0u : 1u) << 10)          // B format F16 / BF16
          | (a_major << 15) | (b_major << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
@@ -204,10 +206,5 @@ TSF_DEV void tmem_st_x32(uint32_t taddr, const uint32_t* r) {
 }
 #undef TSF_R8
 #undef TSF_W8
-
-TSF_DEV uint32_t pack_bf16x2(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x (low half) = lo
-  return *reinterpret_cast<uint32_t*>(&v);
-}
 
 }  // namespace tsf

@@ -31,9 +31,9 @@ struct tsf_handle {
   int device = 0, num_sms = 148;
   ncclComm_t comm = nullptr;
   // workspace (device)
-  __nv_bfloat16 *hi = nullptr, *lo = nullptr;    // X_t planes, [K, N/P, H, d]
-  __nv_bfloat16 *rhi = nullptr, *rlo = nullptr;  // dist: all-to-all receive [P][K/P][N/P][H][d]
-  __nv_bfloat16 *uhi = nullptr, *ulo = nullptr;  // dist: unpacked frame shard [K/P][N][H][d]
+  __half* xt = nullptr;    // X_t = x + T(x) in fp16, [K, N/P, H, d]
+  __half* rxt = nullptr;   // dist: all-to-all receive [P][K/P][N/P][H][d] (also reshard scratch)
+  __half* uxt = nullptr;   // dist: unpacked frame shard [K/P][N][H][d]
   __nv_bfloat16* xdev = nullptr;                 // host API staging
   float* ydev = nullptr;
   std::string err;
@@ -97,7 +97,7 @@ static View spatial_view(int Kl, int N, int H, int d) {  // groups (h, t), axis 
 
 // 4-D tensor map (d, L, A, B) with box (CH, boxL, boxA, boxB).
 static tsf_status make_map(tsf_handle* h, CUtensorMap* m, const void* base, int d, const View& v, int boxL, int boxA,
-                           int boxB) {
+                           int boxB, bool f16) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return fail(h, TSF_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   const int swb = (2 * d < 128) ? 2 * d : 128;
@@ -105,7 +105,7 @@ static tsf_status make_map(tsf_handle* h, CUtensorMap* m, const void* base, int 
   cuuint64_t strides[3] = {(cuuint64_t)v.sL * 2, (cuuint64_t)v.sA * 2, (cuuint64_t)v.sB * 2};
   cuuint32_t box[4] = {(cuuint32_t)(swb / 2), (cuuint32_t)boxL, (cuuint32_t)boxA, (cuuint32_t)boxB};
   cuuint32_t es[4] = {1, 1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+  CUresult r = enc(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, swb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -203,13 +203,13 @@ static tsf_status dispatch_d(tsf_handle* h, bool packed, int win, int epi, cudaS
                              const CUtensorMap& mk, const CUtensorMap& mv, const AttnParams& p) {
   if (packed) {
     switch (epi) {
-      case EPI_BF16: return dispatch_packed_win<D, EPI_BF16, false>(h, win, st, mq, mk, mv, p);
+      case EPI_OUT16: return dispatch_packed_win<D, EPI_OUT16, false>(h, win, st, mq, mk, mv, p);
       case EPI_BLOCK_T: return dispatch_packed_win<D, EPI_BLOCK_T, true>(h, win, st, mq, mk, mv, p);
       default: return dispatch_packed_win<D, EPI_BLOCK_S, true>(h, win, st, mq, mk, mv, p);
     }
   }
   switch (epi) {
-    case EPI_BF16: return launch_flash_t<D, EPI_BF16>(h, st, mq, mk, mv, p);
+    case EPI_OUT16: return launch_flash_t<D, EPI_OUT16>(h, st, mq, mk, mv, p);
     case EPI_BLOCK_T: return launch_flash_t<D, EPI_BLOCK_T>(h, st, mq, mk, mv, p);
     default: return launch_flash_t<D, EPI_BLOCK_S>(h, st, mq, mk, mv, p);
   }
@@ -217,17 +217,16 @@ static tsf_status dispatch_d(tsf_handle* h, bool packed, int win, int epi, cudaS
 
 // Attention over one view: q/k/v (q == k == v for the block stages).
 static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, const void* k, const void* vv, int epi,
-                                void* o, void* o2, const void* res_lo, float* y, cudaStream_t st) {
+                                void* o, float* y, cudaStream_t st) {
   const int d = h->d;
   if ((long long)v.A * v.B == 0 || v.L == 0) return TSF_OK;
   AttnParams p{};
   p.L = v.L; p.A = v.A; p.B = v.B;
   p.sL = v.sL; p.sA = v.sA; p.sB = v.sB;
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
-  p.o = reinterpret_cast<__nv_bfloat16*>(o);
-  p.o2 = reinterpret_cast<__nv_bfloat16*>(o2);
-  p.res_lo = reinterpret_cast<const __nv_bfloat16*>(res_lo);
+  p.o = o;
   p.y = y;
+  const bool f16 = (epi == EPI_BLOCK_S);
   const bool packed = v.L <= 128;
   int win = 128;
   CUtensorMap mq, mk, mv;
@@ -245,15 +244,15 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
     if (tiles > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "too many tiles");
     p.num_tiles = (int)tiles;
     win = (32 % v.L == 0) ? 32 : (64 % v.L == 0) ? 64 : 128;
-    if ((s = make_map(h, &mq, q, d, v, v.L, Ab, Bb)) != TSF_OK) return s;
-    if ((s = make_map(h, &mk, k, d, v, v.L, Ab, Bb)) != TSF_OK) return s;
-    if ((s = make_map(h, &mv, vv, d, v, v.L, Ab, Bb)) != TSF_OK) return s;
+    if ((s = make_map(h, &mq, q, d, v, v.L, Ab, Bb, f16)) != TSF_OK) return s;
+    if ((s = make_map(h, &mk, k, d, v, v.L, Ab, Bb, f16)) != TSF_OK) return s;
+    if ((s = make_map(h, &mv, vv, d, v, v.L, Ab, Bb, f16)) != TSF_OK) return s;
   } else {
     p.n_qpairs = (v.L + 255) / 256;
     p.nkv = (v.L + 127) / 128;
-    if ((s = make_map(h, &mq, q, d, v, 128, 1, 1)) != TSF_OK) return s;
-    if ((s = make_map(h, &mk, k, d, v, 128, 1, 1)) != TSF_OK) return s;
-    if ((s = make_map(h, &mv, vv, d, v, 128, 1, 1)) != TSF_OK) return s;
+    if ((s = make_map(h, &mq, q, d, v, 128, 1, 1, f16)) != TSF_OK) return s;
+    if ((s = make_map(h, &mk, k, d, v, 128, 1, 1, f16)) != TSF_OK) return s;
+    if ((s = make_map(h, &mv, vv, d, v, 128, 1, 1, f16)) != TSF_OK) return s;
   }
   switch (d) {
     case 32: return dispatch_d<32>(h, packed, win, epi, st, mq, mk, mv, p);
@@ -311,11 +310,11 @@ static tsf_status check_shape(int K, int N, int H, int d, int world) {
 
 static tsf_status alloc_workspace(tsf_handle* h) {
   const size_t El = (size_t)h->K * (h->N / h->world) * h->H * h->d;  // token-shard elements
-  auto a = [&](__nv_bfloat16** p, size_t n) -> bool {
-    return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(__nv_bfloat16)) == cudaSuccess;
+  auto a = [&](__half** p, size_t n) -> bool {
+    return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(__half)) == cudaSuccess;
   };
-  bool ok = a(&h->hi, El) && a(&h->lo, El);
-  if (ok && h->world > 1) ok = a(&h->rhi, El) && a(&h->rlo, El) && a(&h->uhi, El) && a(&h->ulo, El);
+  bool ok = a(&h->xt, El);
+  if (ok && h->world > 1) ok = a(&h->rxt, El) && a(&h->uxt, El);
   if (!ok) {
     cudaGetLastError();
     return fail(nullptr, TSF_ERR_NOMEM, "workspace cudaMalloc failed");
@@ -324,8 +323,7 @@ static tsf_status alloc_workspace(tsf_handle* h) {
 }
 
 static void free_workspace(tsf_handle* h) {
-  for (void* p : {(void*)h->hi, (void*)h->lo, (void*)h->rhi, (void*)h->rlo, (void*)h->uhi, (void*)h->ulo,
-                  (void*)h->xdev, (void*)h->ydev})
+  for (void* p : {(void*)h->xt, (void*)h->rxt, (void*)h->uxt, (void*)h->xdev, (void*)h->ydev})
     if (p) cudaFree(p);
 }
 
@@ -441,7 +439,7 @@ tsf_status tsf_temporal_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k
   if (s != TSF_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   StageTimer tm(h, st, 0);
-  s = run_attention(h, temporal_view(h->K, Nl, h->H, h->d), q, k, v, EPI_BF16, o, nullptr, nullptr, nullptr, st);
+  s = run_attention(h, temporal_view(h->K, Nl, h->H, h->d), q, k, v, EPI_OUT16, o, nullptr, st);
   tm.done();
   return s;
 }
@@ -456,28 +454,26 @@ tsf_status tsf_spatial_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k,
   if (s != TSF_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   StageTimer tm(h, st, 1);
-  s = run_attention(h, spatial_view(Kl, h->N, h->H, h->d), q, k, v, EPI_BF16, o, nullptr, nullptr, nullptr, st);
+  s = run_attention(h, spatial_view(Kl, h->N, h->H, h->d), q, k, v, EPI_OUT16, o, nullptr, st);
   tm.done();
   return s;
 }
 
-// X_t token-sharded planes (hi, lo) -> frame-sharded planes, via one grouped
-// NCCL send/recv round (bytes, bit-exact) and the unpack kernel.
+// X_t token shard -> frame shard: one grouped NCCL send/recv round (bytes,
+// bit-exact) and the unpack kernel.
 static tsf_status all_to_all_xt(tsf_handle* h, cudaStream_t st) {
   const int P = h->world, Kc = h->K / P, Nc = h->N / P;
-  const size_t chunk = (size_t)Kc * Nc * h->H * h->d * 2;  // bytes per peer per plane
+  const size_t chunk = (size_t)Kc * Nc * h->H * h->d * 2;  // bytes per peer
   TSF_NCCL(h, ncclGroupStart());
   for (int p = 0; p < P; ++p) {
-    TSF_NCCL(h, ncclSend((const char*)h->hi + p * chunk, chunk, ncclUint8, p, h->comm, st));
-    TSF_NCCL(h, ncclSend((const char*)h->lo + p * chunk, chunk, ncclUint8, p, h->comm, st));
-    TSF_NCCL(h, ncclRecv((char*)h->rhi + p * chunk, chunk, ncclUint8, p, h->comm, st));
-    TSF_NCCL(h, ncclRecv((char*)h->rlo + p * chunk, chunk, ncclUint8, p, h->comm, st));
+    TSF_NCCL(h, ncclSend((const char*)h->xt + p * chunk, chunk, ncclUint8, p, h->comm, st));
+    TSF_NCCL(h, ncclRecv((char*)h->rxt + p * chunk, chunk, ncclUint8, p, h->comm, st));
   }
   TSF_NCCL(h, ncclGroupEnd());
   const int vecs = h->H * h->d * 2 / 16;
   const long long items = (long long)P * Kc * Nc * vecs;
-  reshard_perm_kernel<true><<<grid_for(h, items), 256, 0, st>>>((const uint4*)h->rhi, (uint4*)h->uhi,
-                                                                (const uint4*)h->rlo, (uint4*)h->ulo, P, Kc, Nc, vecs);
+  reshard_perm_kernel<true><<<grid_for(h, items), 256, 0, st>>>((const uint4*)h->rxt, (uint4*)h->uxt, nullptr,
+                                                                nullptr, P, Kc, Nc, vecs);
   TSF_CUDA(h, cudaGetLastError());
   h->launches++;
   return TSF_OK;
@@ -492,26 +488,24 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
   tsf_status s = check_ptrs(h, {x}, y, in_bytes, out_bytes);
   if (s != TSF_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
-  // temporal stage: X_t = x + T(x, x, x) -> (hi, lo)
+  // temporal stage: X_t = x + T(x, x, x), stored fp16
   {
     StageTimer tm(h, st, 0);
-    s = run_attention(h, temporal_view(h->K, Nl, h->H, h->d), x, x, x, EPI_BLOCK_T, h->hi, h->lo, nullptr, nullptr,
-                      st);
+    s = run_attention(h, temporal_view(h->K, Nl, h->H, h->d), x, x, x, EPI_BLOCK_T, h->xt, nullptr, st);
     tm.done();
     if (s != TSF_OK) return s;
   }
-  const __nv_bfloat16 *shi = h->hi, *slo = h->lo;
+  const __half* sxt = h->xt;
   if (P > 1) {
     StageTimer tm(h, st, 2);
     s = all_to_all_xt(h, st);
     tm.done();
     if (s != TSF_OK) return s;
-    shi = h->uhi;
-    slo = h->ulo;
+    sxt = h->uxt;
   }
-  // spatial stage: y = X_t + S(hi, hi, hi), residual hi + lo
+  // spatial stage: y = X_t + S(X_t, X_t, X_t)
   StageTimer tm(h, st, 1);
-  s = run_attention(h, spatial_view(Kl, h->N, h->H, h->d), shi, shi, shi, EPI_BLOCK_S, nullptr, nullptr, slo, y, st);
+  s = run_attention(h, spatial_view(Kl, h->N, h->H, h->d), sxt, sxt, sxt, EPI_BLOCK_S, nullptr, y, st);
   tm.done();
   return s;
 }
@@ -569,20 +563,20 @@ tsf_status tsf_reshard(tsf_handle* h, int dir, const tsf_bf16* in, tsf_bf16* out
     TSF_NCCL(h, ncclGroupStart());
     for (int p = 0; p < P; ++p) {
       TSF_NCCL(h, ncclSend((const char*)in + p * chunk, chunk, ncclUint8, p, h->comm, st));
-      TSF_NCCL(h, ncclRecv((char*)h->rhi + p * chunk, chunk, ncclUint8, p, h->comm, st));
+      TSF_NCCL(h, ncclRecv((char*)h->rxt + p * chunk, chunk, ncclUint8, p, h->comm, st));
     }
     TSF_NCCL(h, ncclGroupEnd());
-    reshard_perm_kernel<true><<<grid_for(h, items), 256, 0, st>>>((const uint4*)h->rhi, (uint4*)out, nullptr,
+    reshard_perm_kernel<true><<<grid_for(h, items), 256, 0, st>>>((const uint4*)h->rxt, (uint4*)out, nullptr,
                                                                   nullptr, P, Kc, Nc, vecs);
   } else {
     // pack [Kc][N] -> [P][Kc][Nc], send block p to peer p; the received
     // blocks [P][Kc][Nc] are exactly the token shard [K][Nc]
-    reshard_perm_kernel<false><<<grid_for(h, items), 256, 0, st>>>((const uint4*)in, (uint4*)h->rhi, nullptr,
+    reshard_perm_kernel<false><<<grid_for(h, items), 256, 0, st>>>((const uint4*)in, (uint4*)h->rxt, nullptr,
                                                                    nullptr, P, Kc, Nc, vecs);
     TSF_CUDA(h, cudaGetLastError());
     TSF_NCCL(h, ncclGroupStart());
     for (int p = 0; p < P; ++p) {
-      TSF_NCCL(h, ncclSend((const char*)h->rhi + p * chunk, chunk, ncclUint8, p, h->comm, st));
+      TSF_NCCL(h, ncclSend((const char*)h->rxt + p * chunk, chunk, ncclUint8, p, h->comm, st));
       TSF_NCCL(h, ncclRecv((char*)out + p * chunk, chunk, ncclUint8, p, h->comm, st));
     }
     TSF_NCCL(h, ncclGroupEnd());
