@@ -1,0 +1,309 @@
+"""Benchmark of the factorized space-time attention block (one "step" = one
+tsf_spacetime_block over a [K, N, H, d] synthetic field: temporal attention,
+[all-to-all], spatial attention, residuals).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl tsf|reference]
+
+N = 1: BASELINE.json configs[1] (C2: K=8, N=4096, H=16, d=64).  N > 1 (torchrun,
+one process per GPU, NCCL): weak scaling with C2 per GPU, K = 8 * N frames,
+x token-sharded in, y frame-sharded out, one all-to-all per step.
+
+Prints ONE JSON line on rank 0 (the driver's contract).
+--impl reference times the fp64 CPU oracle on bounded samples of the same
+workload (the tier's reference arm) on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "space-time tokens/s per attention layer"
+UNIT = "tokens/s"
+BASE = dict(K=8, N=4096, H=16, d=64)          # BASELINE.json configs[1] (C2)
+L2_BYTES = 126 * 2 ** 20
+
+
+def peaks():
+    """MEASURED_PEAKS.json (driver-written), else the profiling guide's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return dict(tflops=m["bf16_tflops"], tflops_sustained=m.get("bf16_tflops_sustained"),
+                    hbm=m["hbm_gbs"], source="MEASURED_PEAKS.json (measured)")
+    except Exception:
+        return dict(tflops=1590.0, tflops_sustained=1400.0, hbm=6650.0,
+                    source="B200_PROFILING.md fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+                for n, v in zip(names, f[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                pass
+        load = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm), "note": getattr(self, "note", "timed region")}
+
+
+def traffic_from_profiles(kernel_tag: str):
+    """dram bytes per launch of the dominant kernel from a committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(kernel_tag)
+    except Exception:
+        return None
+
+
+def cpu_baseline(K, N, H, d, seconds=12.0, label="oracle"):
+    """Time the fp64 oracle (as it stands) on host cores: full (t, h) planes of the
+    block, i.e. y[t, :, h, :], until about `seconds` of CPU work."""
+    import numpy as np
+    import oracle
+    import synth
+    cores = len(os.sched_getaffinity(0))
+    frames = list(range(K))
+    x = synth.bf16_bits_to_f64(synth.make_x(K, N, H, d, seed=0, frames=frames))
+    planes, t0 = 0, time.perf_counter()
+    order = [(t, h) for h in range(H) for t in range(K)]
+    while True:
+        t, h = order[planes % len(order)]
+        oracle.block_plane(x, t, h)
+        planes += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or planes >= 4 * len(order):
+            break
+    tokens = planes * N / H          # a plane is 1/H of the work of N tokens
+    return {"value": tokens / el, "unit": UNIT, "cores": cores, "kind": label,
+            "sample": f"{planes} full (t,h) planes y[t,:,h,:] of the block at K={K} N={N} H={H} d={d} "
+                      f"(= {tokens:.0f} token-equivalents) in {el:.1f} s, numpy fp64, BLAS threads = cores"}
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the fp64 oracle on bounded samples, rank 0 only."""
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    import synth
+    K, N, H, d = BASE["K"] * world, BASE["N"], BASE["H"], BASE["d"]
+    x = synth.bf16_bits_to_f64(synth.make_x(K, N, H, d, seed=0, frames=range(min(K, 8 * world))))
+    order = [(t, h) for h in range(H) for t in range(x.shape[0])]
+    for i in range(args.warmup):
+        oracle.block_plane(x, *order[i % len(order)])
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        oracle.block_plane(x, *order[(args.warmup + i) % len(order)])
+    el = time.perf_counter() - t0
+    tokens = args.steps * N / H
+    value = tokens / el
+    cores = len(os.sched_getaffinity(0))
+    sample = (f"one full (t,h) plane y[t,:,h,:] of the block per step (N/H = {N // H} token-equivalents), "
+              f"K={K} N={N} H={H} d={d}, numpy fp64")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(K, N, H, d, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(K, N, H, d, world):
+    return {"workload": f"C2 per GPU (BASELINE.json configs[1]): K={K} frames (8 per GPU), N={N} tokens "
+                        f"(64x64 lat-lon patches), H={H}, d={d}, batch 1; factorized block temporal->spatial",
+            "K": K, "N": N, "H": H, "d": d, "global_batch": 1, "seq_len": K * N,
+            "parallelism": f"axis-sharded x{world} (temporal by token, spatial by frame, 1 all-to-all)"
+            if world > 1 else "single GPU",
+            "l2": "rotating input/output sets larger than L2 (see l2_sets)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="tsf", choices=["tsf", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import synth
+    import paper_2604_16590_b200 as tsf
+
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+    K, N, H, d = BASE["K"] * world, BASE["N"], BASE["H"], BASE["d"]
+    layer = tsf.Layer(K, N, H, d, group=group)
+    Nl, Kl = N // world, K // world
+
+    # inputs: this rank's token shard; R rotating sets so a step never finds its
+    # input or output in L2 (each set 2*E + 4*E bytes per rank > L2 / R)
+    xs_bits = synth.make_x(K, N, H, d, seed=0, tokens=slice(rank * Nl, (rank + 1) * Nl))
+    x0 = synth.bits_to_torch(xs_bits, "cuda")
+    set_bytes = x0.numel() * 2 + Kl * N * H * d * 4
+    R = max(2, int(np.ceil(3 * L2_BYTES / set_bytes)))
+    xs = [x0] + [x0.clone() for _ in range(R - 1)]
+    ys = [torch.empty(layer.frame_shard_shape, dtype=torch.float32, device="cuda") for _ in range(R)]
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for i in range(args.warmup):
+        layer.block(xs[i % R], out=ys[i % R])
+    torch.cuda.synchronize()
+    barrier()
+
+    launches_per_step = layer.last_launch_count()
+    layer.set_timing(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for i in range(args.steps):
+            layer.block(xs[i % R], out=ys[i % R])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    if len(clk.lines) < 5:
+        # timed region too short for nvidia-smi: sample clocks over a ~1 s
+        # repeat of the same step loop (untimed)
+        reps = max(1, int(1000.0 / max(ms, 1e-3)))
+        with ClockSampler(local) as clk:
+            for _ in range(reps):
+                for i in range(args.steps):
+                    layer.block(xs[i % R], out=ys[i % R])
+            torch.cuda.synchronize()
+        clk.note = f"sampled over a {reps}x repeat of the timed loop"
+    st_ms = {s: layer.stage_ms(s) for s in (tsf.STAGE_TEMPORAL, tsf.STAGE_SPATIAL, tsf.STAGE_RESHARD)}
+    layer.set_timing(False)
+
+    # end to end through the C ABI with HOST buffers (pinned), copies timed
+    xh = xs[0].cpu().pin_memory()
+    yh = torch.empty(layer.frame_shard_shape, dtype=torch.float32).pin_memory()
+    e2e_steps = max(3, min(args.steps, 50))
+    layer.block_host(xh, yh)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        layer.block_host(xh, yh)
+    barrier()
+    e2e_s = time.perf_counter() - t0
+
+    # max over ranks
+    vals = torch.tensor([ms, e2e_s, st_ms[1][0], st_ms[0][0], st_ms[2][0]], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms, e2e_s, sp_ms, tp_ms, rs_ms = vals.tolist()
+
+    if rank == 0:
+        pk = peaks()
+        tokens = K * N
+        step_ms = ms / args.steps
+        value = tokens * args.steps / (ms / 1e3)
+        F = tsf.flops(K, N, H, d)
+        # dominant kernel: the spatial flash-attention kernel; algorithmic flops
+        # per launch = 4 H d Kl N^2 (QK^T + PV) on this rank
+        n_sp = st_ms[1][1]
+        sp_launch_ms = sp_ms / max(n_sp, 1)
+        sp_flops = 4 * H * d * Kl * N * N
+        achieved = sp_flops / (sp_launch_ms / 1e3) / 1e12
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": dict(workload_config(K, N, H, d, world), l2_sets=R),
+            "tflops": F / (step_ms / 1e3) / 1e12,
+            "tflops_frac_of_measured": F / (step_ms / 1e3) / 1e12 / pk["tflops"],
+            "roofline": {"bound": "tensor", "kernel": "attn_flash_kernel<64, EPI_BLOCK_S> (spatial stage)",
+                         "achieved": achieved, "peak": pk["tflops"], "unit": "TFLOP/s",
+                         "frac": achieved / pk["tflops"], "traffic": traffic_from_profiles("spatial_C2"),
+                         "peak_source": pk["source"] + " bf16 burst (fp16 operands: same nominal rate)",
+                         "algorithmic_flops_per_launch": sp_flops, "launch_ms": sp_launch_ms,
+                         "stage_ms": {"temporal": tp_ms / max(st_ms[0][1], 1), "spatial": sp_launch_ms,
+                                      "reshard": rs_ms / max(st_ms[2][1], 1) if world > 1 else 0.0}},
+            "e2e": {"value": tokens * e2e_steps / e2e_s, "unit": UNIT,
+                    "h2d_bytes_per_step": xh.numel() * 2, "d2h_bytes_per_step": yh.numel() * 4},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+        }
+        if world > 1:
+            a2a_bytes = xs[0].numel() * 2 * (world - 1) / world
+            rs_launch_ms = rs_ms / max(st_ms[2][1], 1)
+            algbw = a2a_bytes / (rs_launch_ms / 1e3) / 1e9
+            line["a2a"] = {"bytes_sent_per_rank": a2a_bytes, "ms_incl_unpack": rs_launch_ms, "algbw_GBs": algbw,
+                           "busbw_GBs": algbw * (world - 1) / world, "nvlink_GBs_per_dir": 900}
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(8, N, H, d)
+        print(json.dumps(line), flush=True)
+    layer.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
