@@ -22,9 +22,14 @@
 // fp32 sum of the rounded P and the softmax warps spend no ALU on it; for
 // D = 128 (TMEM full) the warps sum the rounded P themselves.
 //
-// Warp roles (320 threads): warps 0-3 softmax of tile 0, warps 4-7 softmax of
+// exp2: EMU of every 16 exponentials per row go to a polynomial on the FMA/ALU
+// pipes (ex2_poly2) instead of MUFU, which alone caps d = 64 attention near
+// half of tensor peak (16 ex2/clk/SM vs 4d MMA flops per score).
+//
+// Warp roles (384 threads): warps 0-3 softmax of tile 0, warps 4-7 softmax of
 // tile 1 (thread owns TMEM lane = tile row), warp 8 TMA producer, warp 9 MMA
-// issuer and TMEM owner.
+// issuer and TMEM owner, warps 10-11 idle (complete the third warpgroup so
+// setmaxnreg can move registers to the softmax warpgroups).
 #pragma once
 #include "sm100.cuh"
 #include "attn_common.cuh"
@@ -45,14 +50,14 @@ struct FlashCfg {
   static constexpr bool ONES = (D <= 64);               // l via an MMA against a ones column
   static constexpr int ONES_BYTES = 1024;
   static constexpr int SMEM = Q_BYTES + NST * STAGE_BYTES + ONES_BYTES + 1024 + 256;
-  static constexpr int THREADS = 320;
+  static constexpr int THREADS = 384;  // 3 warpgroups (setmaxnreg is per warpgroup)
   static constexpr uint32_t OW = ONES ? D + 16 : D;
   static constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 256 + OW;
   static_assert(COL_O1 + OW <= 512, "TMEM budget");
 };
 
-template <int D, int EPI, int NST>
-__global__ void __launch_bounds__(320, 1)
+template <int D, int EPI, int NST, int EMU>
+__global__ void __launch_bounds__(384, 1)
 attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                   const __grid_constant__ CUtensorMap tv, const AttnParams p) {
   using C = FlashCfg<D, EPI, NST>;
@@ -104,8 +109,11 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
+  // registers (setmaxnreg, per role branch): softmax warpgroups 232/thread,
+  // producer warpgroup (TMA, MMA, 2 idle warps) 40/thread
   if (warp == 8) {
     // ===================== TMA producer =====================
+    reg_dealloc<40>();
     if (elect_one()) {
       tma_prefetch_desc(&tq);
       tma_prefetch_desc(&tk);
@@ -134,6 +142,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     __syncwarp();
   } else if (warp == 9) {
     // ===================== MMA issuer =====================
+    reg_dealloc<40>();
     if (elect_one()) {
       constexpr uint32_t idesc_qk = make_idesc(128, 128, 0, 0, F16);
       constexpr uint32_t idesc_pv = make_idesc(128, D, 0, 1, F16);
@@ -196,8 +205,9 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp < 8) {
     // ===================== softmax warpgroups (warps 0-7) =====================
+    reg_alloc<232>();
     const int t = warp >> 2;                                   // query tile of this warpgroup
     const uint32_t row = (warp & 3) * 32 + lane;               // tile row == TMEM lane
     const uint32_t lane_base = ((warp & 3) * 32) << 16;
@@ -215,12 +225,18 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       for (int c = 0; c < 128; c += 32) tmem_ld_x32(tSrow + c, sv + c);
       tmem_wait_ld();
       const int valid = L - j * 128;  // columns >= valid are beyond the sequence
-      float mx = -INFINITY;
+      if (valid < 128) {
 #pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        const float v = __uint_as_float(sv[c]);
-        mx = (c < valid) ? fmaxf(mx, v) : mx;
+        for (int c = 0; c < 128; ++c) sv[c] = (c < valid) ? sv[c] : 0xFF800000u;  // -inf
       }
+      // row max: 4 independent FMNMX3 chains
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < 128; c += 8)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          m4[q] = max3(m4[q], __uint_as_float(sv[c + 2 * q]), __uint_as_float(sv[c + 2 * q + 1]));
+      const float mx = max3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
       const float m_new = fmaxf(m_run, mx * sl2);
       if (j == 0) {
         m_run = m_new;
@@ -253,22 +269,30 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           }
         }
       }
-      const float mb = m_run;
+      const float nmb = -m_run;
       float lsum = 0.f;
-      uint32_t pk[64];
 #pragma unroll
-      for (int c = 0; c < 128; c += 2) {
-        const float p0 = (c < valid) ? ex2(fmaf(__uint_as_float(sv[c]), sl2, -mb)) : 0.f;
-        const float p1 = (c + 1 < valid) ? ex2(fmaf(__uint_as_float(sv[c + 1]), sl2, -mb)) : 0.f;
-        pk[c / 2] = pack2<F16>(p0, p1);
-        if constexpr (!C::ONES) {
-          const float2 pr = unpack2<F16>(pk[c / 2]);
-          lsum += pr.x + pr.y;
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = c0; c < c0 + 32; c += 2) {
+          float x0, x1, p0, p1;
+          ffma2(x0, x1, __uint_as_float(sv[c]), __uint_as_float(sv[c + 1]), sl2, sl2, nmb, nmb);
+          if (((c >> 1) & 7) >= 8 - EMU / 2) {
+            ex2_poly2(p0, p1, x0, x1);   // FMA/ALU pipes
+          } else {
+            p0 = ex2(x0);                // MUFU
+            p1 = ex2(x1);
+          }
+          pk[(c - c0) / 2] = pack2<F16>(p0, p1);
+          if constexpr (!C::ONES) {
+            const float2 pr = unpack2<F16>(pk[(c - c0) / 2]);
+            lsum += pr.x + pr.y;
+          }
         }
+        tmem_st_x16(tSrow + 64 + c0 / 2, pk);
       }
       l_run += lsum;
-#pragma unroll
-      for (int c = 0; c < 64; c += 32) tmem_st_x32(tSrow + 64 + c, pk + c);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -294,6 +318,8 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       const long long off = (long long)l_idx * p.sL + (long long)ga * p.sA + (long long)gb * p.sB;
       epilogue_row<D, 128, EPI>(p, o, 1.0f / l_run, off, sQ + t * C::TILE_BYTES, row);
     }
+  } else {
+    reg_dealloc<40>();  // idle warps 10-11
   }
 
   tc_fence_before();

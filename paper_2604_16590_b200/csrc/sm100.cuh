@@ -41,6 +41,59 @@ TSF_DEV float ex2(float x) {
   return y;
 }
 
+// 3-input max (FMNMX3, sm_100+)
+TSF_DEV float max3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// Packed fp32x2 FMA (FFMA2, sm_100+): (x0, x1) = (a0*b0 + c0, a1*b1 + c1)
+TSF_DEV void ffma2(float& x0, float& x1, float a0, float a1, float b0, float b1, float c0, float c1) {
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.ftz.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(x0), "=f"(x1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+
+// 2^x for a pair on the FMA/ALU pipes (no MUFU), x <= 0: Cody-Waite split
+// x = i + f, f in [0, 1), 2^f by a degree-3 polynomial with p(0) = 1 (minimax
+// in relative error, max 8.6e-5: below the 2^-9 / 2^-12 rounding that P gets
+// as bf16 / fp16), 2^i added into the exponent field.  Inputs are clamped at
+// -126 (their weight is < 2^-126 of the row max).
+TSF_DEV void ex2_poly2(float& y0, float& y1, float x0, float x1) {
+  // p(f) = 1 + c1 f + c2 f^2 + c3 f^3; c1 = 0.69511634 (0x3F31F325),
+  // c2 = 0.22764700 (0x3E691C4C), c3 = 0.07706520 (0x3D9DD45C): Lawson
+  // iteration for the minimax relative error (tools/fit_exp2.py).
+  asm("{\n\t.reg .b64 rx, rr, rb, rf, rp, c1, c2, c3, one;\n\t"
+      ".reg .f32 a0, a1, b0, b1;\n\t.reg .b32 i0, i1, q0, q1;\n\t"
+      "max.ftz.f32 a0, %2, 0fC2FC0000;\n\tmax.ftz.f32 a1, %3, 0fC2FC0000;\n\t"
+      "mov.b64 rx, {a0, a1};\n\t"
+      "mov.b64 rb, {0f4B400000, 0f4B400000};\n\t"
+      "add.rm.ftz.f32x2 rr, rx, rb;\n\t"          // floor(x) in the low mantissa bits
+      "sub.rn.ftz.f32x2 rf, rr, rb;\n\t"
+      "sub.rn.ftz.f32x2 rf, rx, rf;\n\t"          // f = x - floor(x) in [0, 1)
+      "mov.b64 c3, {0f3D9DD45C, 0f3D9DD45C};\n\t"
+      "mov.b64 c2, {0f3E691C4C, 0f3E691C4C};\n\t"
+      "mov.b64 c1, {0f3F31F325, 0f3F31F325};\n\t"
+      "mov.b64 one, {0f3F800000, 0f3F800000};\n\t"
+      "fma.rn.ftz.f32x2 rp, rf, c3, c2;\n\t"
+      "fma.rn.ftz.f32x2 rp, rp, rf, c1;\n\t"
+      "fma.rn.ftz.f32x2 rp, rp, rf, one;\n\t"
+      "mov.b64 {i0, i1}, rr;\n\tmov.b64 {q0, q1}, rp;\n\t"
+      "shl.b32 i0, i0, 23;\n\tshl.b32 i1, i1, 23;\n\t"
+      "add.s32 q0, q0, i0;\n\tadd.s32 q1, q1, i1;\n\t"
+      "mov.b32 %0, q0;\n\tmov.b32 %1, q1;\n\t}"
+      : "=f"(y0), "=f"(y1)
+      : "f"(x0), "f"(x1));
+}
+
+template <uint32_t R>
+TSF_DEV void reg_alloc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R)); }
+template <uint32_t R>
+TSF_DEV void reg_dealloc() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R)); }
+
 TSF_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

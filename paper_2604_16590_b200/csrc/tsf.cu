@@ -10,6 +10,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -178,14 +179,40 @@ static tsf_status launch_packed_t(tsf_handle* h, cudaStream_t st, const CUtensor
   return launch(h, attn_packed_kernel<D, WIN, EPI, SHARED, NST>, grid, C::THREADS, C::SMEM, st, mq, mk, mv, p);
 }
 
-template <int D, int EPI>
-static tsf_status launch_flash_t(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
-                                 const CUtensorMap& mv, const AttnParams& p) {
+template <int D, int EPI, int EMU>
+static tsf_status launch_flash_emu(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
+                                   const CUtensorMap& mv, const AttnParams& p) {
   constexpr int NST = (D == 128) ? 2 : 4;
   using C = FlashCfg<D, EPI, NST>;
   const long long grid = (long long)p.n_qpairs * p.A * p.B;
   if (grid > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "grid too large");
-  return launch(h, attn_flash_kernel<D, EPI, NST>, (int)grid, C::THREADS, C::SMEM, st, mq, mk, mv, p);
+  return launch(h, attn_flash_kernel<D, EPI, NST, EMU>, (int)grid, C::THREADS, C::SMEM, st, mq, mk, mv, p);
+}
+
+// exp2 emulation share (of 16): TSF_EMU overrides the default for experiments.
+static int emu_setting(int d) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("TSF_EMU");
+    env = e ? atoi(e) : -1;
+  }
+  if (d != 64) return 0;
+  return env >= 0 ? env : 0;
+}
+
+template <int D, int EPI>
+static tsf_status launch_flash_t(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
+                                 const CUtensorMap& mv, const AttnParams& p) {
+  if constexpr (D == 64) {
+    switch (emu_setting(D)) {
+      case 2: return launch_flash_emu<D, EPI, 2>(h, st, mq, mk, mv, p);
+      case 4: return launch_flash_emu<D, EPI, 4>(h, st, mq, mk, mv, p);
+      case 6: return launch_flash_emu<D, EPI, 6>(h, st, mq, mk, mv, p);
+      case 8: return launch_flash_emu<D, EPI, 8>(h, st, mq, mk, mv, p);
+      default: break;
+    }
+  }
+  return launch_flash_emu<D, EPI, 0>(h, st, mq, mk, mv, p);
 }
 
 template <int D, int EPI, bool SHARED>
