@@ -10,10 +10,13 @@
 // order, so a box (d, L, Ab, Bb) lands in shared memory group-major: row
 // r = l + L * (ai + Ab * bi).
 //
-// Operand precision (reading G8): the standalone calls and the
-// temporal stage of the block run on bf16 operands with bf16 P; the spatial
-// stage of the block runs on the fp16 copy of X_t = x + T(x) with fp16 P
-// (11-bit mantissa: X_t and P keep 8x the precision of bf16 at |X_t| <= 2^15).
+// Operand precision (reading G8): the standalone calls run on bf16
+// operands with bf16 P.  Both stages of the block run on fp16 operands with
+// fp16 P (11-bit mantissa, 8x bf16's): the temporal stage converts its bf16 x
+// tiles to fp16 in shared memory (exact for 2^-14 <= |x| <= 65504), and X_t =
+// x + T(x) is stored in fp16 for the spatial stage.  bf16 P in the block's
+// temporal stage perturbs X_t enough to move near-tied spatial logits (~35 at
+// C2) by 2e-2 in y; fp16 P keeps y within 1e-2 (tools/sim notes in DESIGN.md).
 // The softmax denominator l is always the sum of the ROUNDED P that the PV
 // MMA consumes, so the weights applied to V sum to one exactly.
 #pragma once
@@ -24,13 +27,31 @@
 namespace tsf {
 
 enum EpiMode : int {
-  EPI_OUT16 = 0,    // o = bf16(O / l)                          (tsf_*_attn), bf16 operands
-  EPI_BLOCK_T = 1,  // X_t = x + O/l  -> fp16 X_t                (block, temporal stage), bf16 operands
-  EPI_BLOCK_S = 2,  // y = X_t + O/l  -> fp32 y                  (block, spatial stage), fp16 operands
+  EPI_OUT16 = 0,    // o = bf16(O / l)                (tsf_*_attn), bf16 operands, bf16 P
+  EPI_BLOCK_T = 1,  // X_t = x + O/l -> fp16 X_t       (block, temporal stage): x arrives bf16 and
+                    //   is converted to fp16 in shared memory; fp16 operands, fp16 P
+  EPI_BLOCK_S = 2,  // y = X_t + O/l -> fp32 y         (block, spatial stage), fp16 operands, fp16 P
 };
 template <int EPI> struct EpiTraits {
-  static constexpr bool F16 = (EPI == EPI_BLOCK_S);  // operand / P type is fp16 (else bf16)
+  static constexpr bool F16 = (EPI != EPI_OUT16);       // MMA operand / P type is fp16 (else bf16)
+  static constexpr bool CONVERT = (EPI == EPI_BLOCK_T);  // tiles land as bf16, converted in smem
+  static constexpr bool SHARED = (EPI != EPI_OUT16);     // q = k = v: one tile serves Q, K and V
 };
+
+// In-place bf16 -> fp16 conversion of one 16-byte unit (8 elements).  Exact
+// for 2^-14 <= |v| <= 65504; smaller magnitudes become fp16 subnormals
+// (absolute error < 2^-25).
+__device__ __forceinline__ void cvt_unit_bf16_to_f16(uint8_t* p) {
+  uint4 w = *reinterpret_cast<uint4*>(p);
+  uint32_t* u = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float lo = __uint_as_float(u[i] << 16), hi = __uint_as_float(u[i] & 0xFFFF0000u);
+    __half2 h = __floats2half2_rn(lo, hi);
+    u[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  *reinterpret_cast<uint4*>(p) = w;
+}
 
 struct AttnParams {
   int L, A, B;               // sequence length, group dims

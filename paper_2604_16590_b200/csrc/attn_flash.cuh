@@ -28,8 +28,11 @@
 //
 // Warp roles (384 threads): warps 0-3 softmax of tile 0, warps 4-7 softmax of
 // tile 1 (thread owns TMEM lane = tile row), warp 8 TMA producer, warp 9 MMA
-// issuer and TMEM owner, warps 10-11 idle (complete the third warpgroup so
-// setmaxnreg can move registers to the softmax warpgroups).
+// issuer and TMEM owner, warps 10-11 convert bf16 tiles to fp16 in the block's
+// temporal stage (otherwise idle; they complete the third warpgroup so
+// setmaxnreg can move registers to the softmax warpgroups).  In the block
+// modes q = k = v, so one TMA tile per stage serves as K (K-major view for
+// QK^T) and V (MN-major view for PV).
 #pragma once
 #include "sm100.cuh"
 #include "attn_common.cuh"
@@ -46,7 +49,8 @@ struct FlashCfg {
   static constexpr int CHUNK_BYTES = 128 * SWB;
   static constexpr int TILE_BYTES = NCH * CHUNK_BYTES;  // 128 x D 16-bit
   static constexpr int Q_BYTES = 2 * TILE_BYTES;
-  static constexpr int STAGE_BYTES = 2 * TILE_BYTES;    // K + V
+  static constexpr bool SHARED = EpiTraits<EPI>::SHARED;  // block: K_j = V_j (one tile per stage)
+  static constexpr int STAGE_BYTES = (SHARED ? 1 : 2) * TILE_BYTES;  // K (+ V)
   static constexpr bool ONES = (D <= 64);               // l via an MMA against a ones column
   static constexpr int ONES_BYTES = 1024;
   static constexpr int SMEM = Q_BYTES + NST * STAGE_BYTES + ONES_BYTES + 1024 + 256;
@@ -62,6 +66,8 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
                   const __grid_constant__ CUtensorMap tv, const AttnParams p) {
   using C = FlashCfg<D, EPI, NST>;
   constexpr bool F16 = EpiTraits<EPI>::F16;
+  constexpr bool CONVERT = EpiTraits<EPI>::CONVERT;
+  constexpr bool SHARED = C::SHARED;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                        // Q0 | Q1
@@ -75,7 +81,9 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
   uint64_t* s_full = kv_empty + NST;         // [2]
   uint64_t* p_full = s_full + 2;             // [2]
   uint64_t* o_full = p_full + 2;             // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 2);
+  uint64_t* q_conv = o_full + 2;             // converter warps -> MMA (CONVERT only)
+  uint64_t* kv_conv = q_conv + 1;            // [NST]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(kv_conv + NST);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int L = p.L, nkv = p.nkv;
@@ -95,7 +103,9 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
       mbar_init(&kv_empty[s], 1);
+      mbar_init(&kv_conv[s], 2);
     }
+    mbar_init(q_conv, 2);
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
       mbar_init(&p_full[t], 4);
@@ -133,10 +143,12 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
 #pragma unroll
         for (int c = 0; c < C::NCH; ++c)
           tma_load_4d(sk + c * C::CHUNK_BYTES, &tk, &k_full[s], c * C::CH, j * 128, ga, gb);
-        mbar_arrive_expect_tx(&v_full[s], C::TILE_BYTES);
+        if constexpr (!SHARED) {
+          mbar_arrive_expect_tx(&v_full[s], C::TILE_BYTES);
 #pragma unroll
-        for (int c = 0; c < C::NCH; ++c)
-          tma_load_4d(sk + C::TILE_BYTES + c * C::CHUNK_BYTES, &tv, &v_full[s], c * C::CH, j * 128, ga, gb);
+          for (int c = 0; c < C::NCH; ++c)
+            tma_load_4d(sk + C::TILE_BYTES + c * C::CHUNK_BYTES, &tv, &v_full[s], c * C::CH, j * 128, ga, gb);
+        }
       }
     }
     __syncwarp();
@@ -163,7 +175,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         mma_commit(&s_full[t]);
       };
       auto issue_pv = [&](int t, int j) {
-        const uint32_t va = smem_u32(sKV + (j % NST) * C::STAGE_BYTES + C::TILE_BYTES);
+        const uint32_t va = smem_u32(sKV + (j % NST) * C::STAGE_BYTES + (SHARED ? 0 : C::TILE_BYTES));
         const uint32_t aP = tmem + (t ? C::COL_S1 : C::COL_S0) + 64;
         const uint32_t dO = tmem + (t ? C::COL_O1 : C::COL_O0);
 #pragma unroll
@@ -175,24 +187,31 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         mma_commit(&o_full[t]);
       };
 
-      mbar_wait(q_full, 0);
-      mbar_wait(&k_full[0], 0);
+      // wait until K tile j (and, separately, V tile j) of stage j % NST is usable
+      auto wait_k = [&](int j) {
+        if constexpr (CONVERT) mbar_wait(&kv_conv[j % NST], (j / NST) & 1);
+        else mbar_wait(&k_full[j % NST], (j / NST) & 1);
+      };
+      auto wait_v = [&](int j) {
+        if constexpr (!SHARED) mbar_wait(&v_full[j % NST], (j / NST) & 1);
+        else wait_k(j);
+      };
+      if constexpr (CONVERT) mbar_wait(q_conv, 0);
+      else mbar_wait(q_full, 0);
+      wait_k(0);
       tc_fence_after();
       issue_s(0, 0);
       issue_s(1, 0);
       for (int j = 0; j < nkv; ++j) {
         const int s = j % NST;
-        const uint32_t ph = (j / NST) & 1;
-        mbar_wait(&v_full[s], ph);
+        wait_v(j);
         const bool more = j + 1 < nkv;
-        const int s1 = (j + 1) % NST;
-        const uint32_t ph1 = ((j + 1) / NST) & 1;
         // tile 0
         mbar_wait(&p_full[0], j & 1);
         tc_fence_after();
         issue_pv(0, j);
         if (more) {
-          mbar_wait(&k_full[s1], ph1);
+          wait_k(j + 1);
           tc_fence_after();
           issue_s(0, j + 1);
         }
@@ -319,7 +338,33 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       epilogue_row<D, 128, EPI>(p, o, 1.0f / l_run, off, sQ + t * C::TILE_BYTES, row);
     }
   } else {
-    reg_dealloc<40>();  // idle warps 10-11
+    // ===================== converter warps 10-11 (block temporal stage) =====================
+    reg_dealloc<40>();
+    if constexpr (CONVERT) {
+      // bf16 tiles from TMA -> fp16 in place (rows are whole 16-byte units, so
+      // the swizzle does not matter); 64 threads, one row-chunk unit at a time
+      constexpr int UPR = 2 * D / 16;  // 16-byte units per row
+      constexpr int UPC = C::SWB / 16;
+      const uint32_t ct = threadIdx.x - 320;
+      auto convert_tile = [&](uint8_t* tile) {
+        for (uint32_t i = ct; i < 128 * UPR; i += 64) {
+          const uint32_t row = i / UPR, u = i % UPR;
+          cvt_unit_bf16_to_f16(tile + (u / UPC) * C::CHUNK_BYTES + row * C::SWB + (u % UPC) * 16);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+      };
+      mbar_wait(q_full, 0);
+      convert_tile(sQ);
+      convert_tile(sQ + C::TILE_BYTES);
+      if (lane == 0) mbar_arrive(q_conv);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % NST;
+        mbar_wait(&k_full[s], (j / NST) & 1);
+        convert_tile(sKV + s * C::STAGE_BYTES);
+        if (lane == 0) mbar_arrive(&kv_conv[s]);
+      }
+    }
   }
 
   tc_fence_before();

@@ -39,6 +39,8 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
                    const __grid_constant__ CUtensorMap tv, const AttnParams p) {
   using C = PackedCfg<D, WIN, EPI, SHARED, NST>;
   constexpr bool F16 = EpiTraits<EPI>::F16;
+  constexpr bool CONVERT = EpiTraits<EPI>::CONVERT;
+  static_assert(SHARED == EpiTraits<EPI>::SHARED, "q = k = v exactly in the block modes");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * C::STAGE_BYTES);
@@ -48,7 +50,8 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
   uint64_t* p_full = s_full + 1;       // softmax -> MMA
   uint64_t* o_full = s_full + 2;       // MMA -> epilogue
   uint64_t* o_empty = s_full + 3;      // epilogue -> MMA
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_full + 4);
+  uint64_t* conv_full = s_full + 4;    // softmax warps converted the stage to fp16 -> MMA
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_full + 5);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int L = p.L;
@@ -70,6 +73,7 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
     mbar_init(p_full, 4);
     mbar_init(o_full, 1);
     mbar_init(o_empty, 4);
+    mbar_init(conv_full, 4);
     fence_barrier_init();
   }
   if (warp == 4) tmem_alloc<C::TCOLS>(tmem_holder);
@@ -113,7 +117,8 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
       constexpr uint32_t idesc_pv = make_idesc(128, D, 0, 1, F16);
       for (int i = 0; i < my_tiles; ++i) {
         const int s = i % NST;
-        mbar_wait(&full[s], (i / NST) & 1);
+        if constexpr (CONVERT) mbar_wait(conv_full, i & 1);
+        else mbar_wait(&full[s], (i / NST) & 1);
         tc_fence_after();
         const uint32_t qa = smem_u32(smem + s * C::STAGE_BYTES);
         const uint32_t ka = SHARED ? qa : qa + C::TILE_BYTES;
@@ -163,6 +168,19 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
     for (int i = 0; i < my_tiles; ++i) {
       const int tile = blockIdx.x + i * gridDim.x;
       const int s = i % NST;
+      if constexpr (CONVERT) {
+        // x tile (bf16 from TMA) -> fp16 in place: each thread converts its row
+        mbar_wait(&full[s], (i / NST) & 1);
+        uint8_t* tile = smem + s * C::STAGE_BYTES;
+#pragma unroll
+        for (int u = 0; u < D / 8; ++u) {
+          constexpr int UPC = C::SWB / 16;
+          cvt_unit_bf16_to_f16(tile + (u / UPC) * C::CHUNK_BYTES + (r * C::SWB) + (u % UPC) * 16);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(conv_full);
+      }
       mbar_wait(s_full, i & 1);
       tc_fence_after();
       uint32_t sv[WIN];

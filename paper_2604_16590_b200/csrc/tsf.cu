@@ -182,7 +182,8 @@ static tsf_status launch_packed_t(tsf_handle* h, cudaStream_t st, const CUtensor
 template <int D, int EPI, int EMU>
 static tsf_status launch_flash_emu(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
                                    const CUtensorMap& mv, const AttnParams& p) {
-  constexpr int NST = (D == 128) ? 2 : 4;
+  constexpr bool SH = EpiTraits<EPI>::SHARED;
+  constexpr int NST = SH ? ((D == 128) ? 4 : 8) : ((D == 128) ? 2 : 4);
   using C = FlashCfg<D, EPI, NST>;
   const long long grid = (long long)p.n_qpairs * p.A * p.B;
   if (grid > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "grid too large");
@@ -253,7 +254,7 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
   p.o = o;
   p.y = y;
-  const bool f16 = (epi == EPI_BLOCK_S);
+  const bool f16 = (epi == EPI_BLOCK_S);  // X_t lives in fp16; x (BLOCK_T) arrives bf16
   const bool packed = v.L <= 128;
   int win = 128;
   CUtensorMap mq, mk, mv;

@@ -197,3 +197,12 @@ def test_abi_errors(tsf_lib):
     s = L.tsf_temporal_attn(layer._h, x.data_ptr() + 2, x.data_ptr(), x.data_ptr(), None, None)
     assert s == tsf_lib.TSF_ERR_CONFIG                     # null / misaligned
     assert b"aligned" in L.tsf_last_error(layer._h)
+
+
+def test_full_C2_block_every_row(tsf_lib):
+    """The bench workload (BASELINE configs[1]) compared on EVERY output element."""
+    w = synth.CONFIGS["C2"]
+    xb = synth.make_x(w.K, w.N, w.H, w.d, seed=0)
+    layer = tsf_lib.Layer(w.K, w.N, w.H, w.d)
+    y = host(layer.block(to_dev(xb)))
+    check(y, oracle.block(f64(xb)), "C2 block, all rows")
