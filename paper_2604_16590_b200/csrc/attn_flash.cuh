@@ -5,17 +5,21 @@
 //
 // One CTA owns two 128-row query tiles of one group and streams the group's
 // K/V in 128-row tiles through an NST-deep TMA ring shared by both query tiles
-// (halves K/V smem/L2 traffic per flop).  The MMA warp ping-pongs
-// S_t = Q_t K_j^T and O_t += P_t V_j between the two tiles so the tensor core
-// works on one tile while the softmax warpgroup of the other runs.
+// (halves K/V smem/L2 traffic per flop).  Each KV tile is consumed in two
+// 64-column sub-steps.  Per query tile t the S accumulator is double-buffered
+// in TMEM (buffers at columns 128 t + {0, 64}); P_t(i) (16-bit pairs, 32
+// columns) overwrites the upper half of the buffer S_t(i) came from, after it
+// has been read into registers.  The MMA warp issues, per sub-step i and tile
+// t: O_t += P_t(i) V(i), then S_t(i+2) into the buffer just released (the
+// tensor pipe executes in order), so while a softmax warpgroup works on S_t(i)
+// the next S_t(i+1) is already resident and the tensor core works on the other
+// tile and on S_t(i+2).  O0, O1 live at columns 256 and 256 + OW, OW = D (+16
+// l columns when D <= 64).
 //
-// TMEM (512 columns): S0 [0,128), S1 [128,256), O0 [256, 256+OW), O1 after
-// it, OW = D (+16 for the l columns when D <= 64).  P_t (16-bit pairs, 64
-// columns) overwrites the upper half of S_t after S_t has been read into
-// registers.  Online softmax in the log2 domain with conditional rescaling:
-// the running max only moves (and O_t is rescaled in TMEM) when a row max
-// grows by more than RESCALE_LOG2; O/l is exact either way because l is
-// accumulated against the same stale max.
+// Online softmax in the log2 domain with conditional rescaling: the running
+// max only moves (and O_t is rescaled in TMEM) when a row max grows by more
+// than RESCALE_LOG2; O/l is exact either way because l is accumulated against
+// the same stale max.
 //
 // Softmax denominator: for D <= 64 the MMA warp also multiplies P_t by a
 // column of ones (an N=16 MMA into the l columns after O_t), so l is the exact
@@ -56,7 +60,9 @@ struct FlashCfg {
   static constexpr int SMEM = Q_BYTES + NST * STAGE_BYTES + ONES_BYTES + 1024 + 256;
   static constexpr int THREADS = 384;  // 3 warpgroups (setmaxnreg is per warpgroup)
   static constexpr uint32_t OW = ONES ? D + 16 : D;
-  static constexpr uint32_t COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 256 + OW;
+  // S buffers: tile t, buffer b at column 128 t + 64 b (64 fp32 columns); P
+  // (64 16-bit values = 32 columns) overwrites the buffer's upper half.
+  static constexpr uint32_t COL_O0 = 256, COL_O1 = 256 + OW;
   static_assert(COL_O1 + OW <= 512, "TMEM budget");
 };
 
@@ -78,15 +84,17 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
   uint64_t* k_full = bars + 1;               // [NST]
   uint64_t* v_full = k_full + NST;           // [NST]
   uint64_t* kv_empty = v_full + NST;         // [NST]
-  uint64_t* s_full = kv_empty + NST;         // [2]
-  uint64_t* p_full = s_full + 2;             // [2]
-  uint64_t* o_full = p_full + 2;             // [2]
-  uint64_t* q_conv = o_full + 2;             // converter warps -> MMA (CONVERT only)
+  uint64_t* s_full = kv_empty + NST;         // [2 tiles][2 buffers]
+  uint64_t* p_full = s_full + 4;             // [2 tiles][2 buffers]
+  uint64_t* o_full = p_full + 4;             // [2] one phase per PV sub-step
+  uint64_t* o_done = o_full + 2;             // [2] last PV of the tile retired
+  uint64_t* q_conv = o_done + 2;             // converter warps -> MMA (CONVERT only)
   uint64_t* kv_conv = q_conv + 1;            // [NST]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(kv_conv + NST);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int L = p.L, nkv = p.nkv;
+  const int nsub = (L + 63) / 64;  // 64-column sub-steps (two per 128-row KV tile)
   const int qp = blockIdx.x % p.n_qpairs;
   const int grp = blockIdx.x / p.n_qpairs;
   const int ga = grp % p.A, gb = grp / p.A;
@@ -106,10 +114,13 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       mbar_init(&kv_conv[s], 2);
     }
     mbar_init(q_conv, 2);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+    }
     for (int t = 0; t < 2; ++t) {
-      mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], 4);
       mbar_init(&o_full[t], 1);
+      mbar_init(&o_done[t], 1);
     }
     fence_barrier_init();
   }
@@ -119,11 +130,11 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  // registers (setmaxnreg, per role branch): softmax warpgroups 232/thread,
-  // producer warpgroup (TMA, MMA, 2 idle warps) 40/thread
+  // registers (setmaxnreg, per role branch): softmax warpgroups 224/thread,
+  // producer warpgroup (TMA, MMA, 2 converter warps) 56/thread
   if (warp == 8) {
     // ===================== TMA producer =====================
-    reg_dealloc<40>();
+    reg_dealloc<56>();
     if (elect_one()) {
       tma_prefetch_desc(&tq);
       tma_prefetch_desc(&tk);
@@ -154,40 +165,44 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     __syncwarp();
   } else if (warp == 9) {
     // ===================== MMA issuer =====================
-    reg_dealloc<40>();
+    reg_dealloc<56>();
     if (elect_one()) {
-      constexpr uint32_t idesc_qk = make_idesc(128, 128, 0, 0, F16);
+      constexpr uint32_t idesc_qk = make_idesc(128, 64, 0, 0, F16);
       constexpr uint32_t idesc_pv = make_idesc(128, D, 0, 1, F16);
       constexpr uint32_t idesc_l = make_idesc(128, 16, 0, 1, F16);
       constexpr uint32_t swz = (C::SWB == 128) ? SWZ_128B : SWZ_64B;
       const uint32_t q_addr = smem_u32(sQ);
       const uint64_t ones_desc = make_sdesc(smem_u32(sOnes), 128, 128, SWZ_NONE);
-      auto issue_s = [&](int t, int j) {
-        const uint32_t ka = smem_u32(sKV + (j % NST) * C::STAGE_BYTES);
+      // S_t(i) = Q_t K_{rows 64i..64i+63}^T  -> S buffer (t, i % 2)
+      auto issue_s = [&](int t, int i) {
+        const uint32_t ka = smem_u32(sKV + ((i >> 1) % NST) * C::STAGE_BYTES) + (i & 1) * 64 * C::SWB;
         const uint32_t qa = q_addr + t * C::TILE_BYTES;
-        const uint32_t dS = tmem + (t ? C::COL_S1 : C::COL_S0);
+        const uint32_t dS = tmem + 128 * t + 64 * (i & 1);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k * 16 / C::CH) * C::CHUNK_BYTES + (k * 16 % C::CH) * 2;
           mma_ss(dS, make_sdesc(qa + off, 16, 8 * C::SWB, swz), make_sdesc(ka + off, 16, 8 * C::SWB, swz),
                  idesc_qk, k > 0);
         }
-        mma_commit(&s_full[t]);
+        mma_commit(&s_full[2 * t + (i & 1)]);
       };
-      auto issue_pv = [&](int t, int j) {
-        const uint32_t va = smem_u32(sKV + (j % NST) * C::STAGE_BYTES + (SHARED ? 0 : C::TILE_BYTES));
-        const uint32_t aP = tmem + (t ? C::COL_S1 : C::COL_S0) + 64;
+      // O_t += P_t(i) V_{rows 64i..64i+63} (+ l_t += P_t(i) 1)
+      auto issue_pv = [&](int t, int i) {
+        const uint32_t va = smem_u32(sKV + ((i >> 1) % NST) * C::STAGE_BYTES + (SHARED ? 0 : C::TILE_BYTES)) +
+                            (i & 1) * 64 * C::SWB;
+        const uint32_t aP = tmem + 128 * t + 64 * (i & 1) + 32;
         const uint32_t dO = tmem + (t ? C::COL_O1 : C::COL_O0);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
           mma_ts(dO, aP + 8 * k, make_sdesc(va + k * 16 * C::SWB, C::CHUNK_BYTES, 8 * C::SWB, swz), idesc_pv, acc);
           if constexpr (C::ONES) mma_ts(dO + D, aP + 8 * k, ones_desc, idesc_l, acc);
         }
         mma_commit(&o_full[t]);
+        if (i == nsub - 1) mma_commit(&o_done[t]);
       };
 
-      // wait until K tile j (and, separately, V tile j) of stage j % NST is usable
+      // K tile j (and, separately, V tile j) of stage j % NST usable
       auto wait_k = [&](int j) {
         if constexpr (CONVERT) mbar_wait(&kv_conv[j % NST], (j / NST) & 1);
         else mbar_wait(&k_full[j % NST], (j / NST) & 1);
@@ -202,72 +217,72 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       tc_fence_after();
       issue_s(0, 0);
       issue_s(1, 0);
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j % NST;
-        wait_v(j);
-        const bool more = j + 1 < nkv;
-        // tile 0
-        mbar_wait(&p_full[0], j & 1);
-        tc_fence_after();
-        issue_pv(0, j);
-        if (more) {
-          wait_k(j + 1);
+      if (nsub > 1) {
+        issue_s(0, 1);
+        issue_s(1, 1);
+      }
+      for (int i = 0; i < nsub; ++i) {
+        const int j = i >> 1;
+        if ((i & 1) == 0) wait_v(j);
+        const bool last_of_tile = (i & 1) || i == nsub - 1;
+        const bool more = i + 2 < nsub;
+        if (more && ((i + 2) & 1) == 0) wait_k((i + 2) >> 1);
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          mbar_wait(&p_full[2 * t + (i & 1)], (i >> 1) & 1);
           tc_fence_after();
-          issue_s(0, j + 1);
+          issue_pv(t, i);
+          if (t == 1 && last_of_tile) mma_commit(&kv_empty[j % NST]);  // K_j/V_j free once retired
+          if (more) issue_s(t, i + 2);   // reuses buffer i % 2 after PV_t(i) (in-order pipe)
         }
-        // tile 1
-        mbar_wait(&p_full[1], j & 1);
-        tc_fence_after();
-        issue_pv(1, j);
-        mma_commit(&kv_empty[s]);  // K_j, V_j no longer read once these MMAs retire
-        if (more) issue_s(1, j + 1);
       }
     }
     __syncwarp();
   } else if (warp < 8) {
     // ===================== softmax warpgroups (warps 0-7) =====================
-    reg_alloc<232>();
+    reg_alloc<224>();
     const int t = warp >> 2;                                   // query tile of this warpgroup
     const uint32_t row = (warp & 3) * 32 + lane;               // tile row == TMEM lane
     const uint32_t lane_base = ((warp & 3) * 32) << 16;
-    const uint32_t tSrow = tmem + lane_base + (t ? C::COL_S1 : C::COL_S0);
+    const uint32_t tSrow = tmem + lane_base + 128 * t;
     const uint32_t tOrow = tmem + lane_base + (t ? C::COL_O1 : C::COL_O0);
     const float sl2 = p.scale_log2;
     float m_run = -INFINITY;  // running max, log2-scaled units
     float l_run = 0.f;        // used when !ONES
 
-    for (int j = 0; j < nkv; ++j) {
-      mbar_wait(&s_full[t], j & 1);
+    for (int i = 0; i < nsub; ++i) {
+      const uint32_t tSb = tSrow + 64 * (i & 1);
+      mbar_wait(&s_full[2 * t + (i & 1)], (i >> 1) & 1);
       tc_fence_after();
-      uint32_t sv[128];
-#pragma unroll
-      for (int c = 0; c < 128; c += 32) tmem_ld_x32(tSrow + c, sv + c);
+      uint32_t sv[64];
+      tmem_ld_x32(tSb, sv);
+      tmem_ld_x32(tSb + 32, sv + 32);
       tmem_wait_ld();
-      const int valid = L - j * 128;  // columns >= valid are beyond the sequence
-      if (valid < 128) {
+      const int valid = L - i * 64;  // columns >= valid are beyond the sequence
+      if (valid < 64) {
 #pragma unroll
-        for (int c = 0; c < 128; ++c) sv[c] = (c < valid) ? sv[c] : 0xFF800000u;  // -inf
+        for (int c = 0; c < 64; ++c) sv[c] = (c < valid) ? sv[c] : 0xFF800000u;  // -inf
       }
       // row max: 4 independent FMNMX3 chains
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < 128; c += 8)
+      for (int c = 0; c < 64; c += 8)
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           m4[q] = max3(m4[q], __uint_as_float(sv[c + 2 * q]), __uint_as_float(sv[c + 2 * q + 1]));
       const float mx = max3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
       const float m_new = fmaxf(m_run, mx * sl2);
-      if (j == 0) {
+      if (i == 0) {
         m_run = m_new;
       } else {
         const bool need = (m_new - m_run) > RESCALE_LOG2;
         if (__any_sync(0xffffffffu, need)) {
           // Move the max for the whole warp (exact for every row); rescale O_t
-          // (and its l columns) once PV_t^{j-1} has retired.
+          // (and its l columns) once PV_t(i-1) has retired.
           const float alpha = ex2(m_run - m_new);
           l_run *= alpha;
           m_run = m_new;
-          mbar_wait(&o_full[t], (j - 1) & 1);
+          mbar_wait(&o_full[t], (i - 1) & 1);
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < D; c += 32) {
@@ -275,7 +290,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
             tmem_ld_x32(tOrow + c, ov);
             tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
             tmem_st_x32(tOrow + c, ov);
           }
           if constexpr (C::ONES) {
@@ -283,7 +298,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
             tmem_ld_x8(tOrow + D, lv);
             tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 8; ++i) lv[i] = __float_as_uint(__uint_as_float(lv[i]) * alpha);
+            for (int e = 0; e < 8; ++e) lv[e] = __float_as_uint(__uint_as_float(lv[e]) * alpha);
             tmem_st_x8(tOrow + D, lv);
           }
         }
@@ -291,7 +306,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       const float nmb = -m_run;
       float lsum = 0.f;
 #pragma unroll
-      for (int c0 = 0; c0 < 128; c0 += 32) {
+      for (int c0 = 0; c0 < 64; c0 += 32) {
         uint32_t pk[16];
 #pragma unroll
         for (int c = c0; c < c0 + 32; c += 2) {
@@ -309,17 +324,17 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
             lsum += pr.x + pr.y;
           }
         }
-        tmem_st_x16(tSrow + 64 + c0 / 2, pk);
+        tmem_st_x16(tSb + 32 + c0 / 2, pk);
       }
       l_run += lsum;
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t]);
+      if (lane == 0) mbar_arrive(&p_full[2 * t + (i & 1)]);
     }
 
     // ---- epilogue ----
-    mbar_wait(&o_full[t], (nkv - 1) & 1);
+    mbar_wait(&o_done[t], 0);
     tc_fence_after();
     float o[D];
 #pragma unroll
@@ -339,7 +354,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     }
   } else {
     // ===================== converter warps 10-11 (block temporal stage) =====================
-    reg_dealloc<40>();
+    reg_dealloc<56>();
     if constexpr (CONVERT) {
       // bf16 tiles from TMA -> fp16 in place (rows are whole 16-byte units, so
       // the swizzle does not matter); 64 threads, one row-chunk unit at a time
