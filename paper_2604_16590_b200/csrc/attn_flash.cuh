@@ -314,11 +314,16 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           ffma2(x0, x1, __uint_as_float(sv[c]), __uint_as_float(sv[c + 1]), sl2, sl2, nmb, nmb);
           if (((c >> 1) & 7) >= 8 - EMU / 2) {
             ex2_poly2(p0, p1, x0, x1);   // FMA/ALU pipes
+            pk[(c - c0) / 2] = pack2<F16>(p0, p1);
+          } else if constexpr (F16) {
+            // fp16 P: exponent of the packed fp16 pair, one MUFU op per two
+            // scores (x <= RESCALE_LOG2 so 2^x <= 256 fits fp16)
+            pk[(c - c0) / 2] = ex2_f16x2(pack2<true>(x0, x1));
           } else {
             p0 = ex2(x0);                // MUFU
             p1 = ex2(x1);
+            pk[(c - c0) / 2] = pack2<F16>(p0, p1);
           }
-          pk[(c - c0) / 2] = pack2<F16>(p0, p1);
           if constexpr (!C::ONES) {
             const float2 pr = unpack2<F16>(pk[(c - c0) / 2]);
             lsum += pr.x + pr.y;

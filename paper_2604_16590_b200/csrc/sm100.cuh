@@ -48,6 +48,13 @@ TSF_DEV float max3(float a, float b, float c) {
   return d;
 }
 
+// 2^x on a packed fp16 pair (one MUFU op for two values)
+TSF_DEV uint32_t ex2_f16x2(uint32_t x) {
+  uint32_t y;
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
 // Packed fp32x2 FMA (FFMA2, sm_100+): (x0, x1) = (a0*b0 + c0, a1*b1 + c1)
 TSF_DEV void ffma2(float& x0, float& x1, float a0, float a1, float b0, float b1, float c0, float c1) {
   asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"

@@ -190,22 +190,26 @@ static tsf_status launch_flash_emu(tsf_handle* h, cudaStream_t st, const CUtenso
   return launch(h, attn_flash_kernel<D, EPI, NST, EMU>, (int)grid, C::THREADS, C::SMEM, st, mq, mk, mv, p);
 }
 
-// exp2 emulation share (of 16): TSF_EMU overrides the default for experiments.
-static int emu_setting(int d) {
+// exp2 emulation share (of 16) for the d = 64 flash kernel: TSF_EMU overrides
+// the default for experiments.  bf16 P (standalone calls) uses fp32 MUFU ex2,
+// where 6/16 on the FMA pipe measured best; fp16 P (block) uses the packed
+// f16x2 MUFU ex2 (two scores per op) and needs no emulation.
+static int emu_setting(int d, int epi) {
   static int env = -2;
   if (env == -2) {
     const char* e = getenv("TSF_EMU");
     env = e ? atoi(e) : -1;
   }
   if (d != 64) return 0;
-  return env >= 0 ? env : 6;  // measured best at C2 (gpurun_out/sweep)
+  if (env >= 0) return env;
+  return epi == EPI_OUT16 ? 6 : 0;
 }
 
 template <int D, int EPI>
 static tsf_status launch_flash_t(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
                                  const CUtensorMap& mv, const AttnParams& p) {
   if constexpr (D == 64) {
-    switch (emu_setting(D)) {
+    switch (emu_setting(D, EPI)) {
       case 2: return launch_flash_emu<D, EPI, 2>(h, st, mq, mk, mv, p);
       case 4: return launch_flash_emu<D, EPI, 4>(h, st, mq, mk, mv, p);
       case 6: return launch_flash_emu<D, EPI, 6>(h, st, mq, mk, mv, p);
