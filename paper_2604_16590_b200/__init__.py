@@ -21,7 +21,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtsf.so")
+LIB_PATH = os.environ.get("TSF_LIB") or os.path.join(_HERE, "libtsf.so")
 
 # status codes (include/tsf.h)
 TSF_OK, TSF_ERR_CONFIG, TSF_ERR_NUMERIC, TSF_ERR_UNSUPPORTED, TSF_ERR_CUDA, TSF_ERR_NCCL, TSF_ERR_NOMEM = \

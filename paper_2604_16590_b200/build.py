@@ -38,14 +38,17 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in SOURCES + HEADERS)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    if not force and not needs_build():
+def build(verbose: bool = False, force: bool = False, trace: bool = False) -> str:
+    """trace=True builds libtsf_trace.so with -DTSF_TRACE (clock64 stamps, diagnostics)."""
+    out = LIB.replace("libtsf.so", "libtsf_trace.so") if trace else LIB
+    if not force and not trace and not needs_build():
         return LIB
     inc, lib = nccl_paths()
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-O2", "-shared", "-cudart", "shared",
            "-I", os.path.join(ROOT, "include"), "-I", inc,
-           "-o", LIB + ".tmp", *SOURCES,
+           *(["-DTSF_TRACE"] if trace else []),
+           "-o", out + ".tmp", *SOURCES,
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
@@ -55,10 +58,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
         raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
     if verbose:
         print(r.stdout, r.stderr, flush=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    build(verbose="--verbose" in sys.argv, force=True)
-    print(LIB)
+    print(build(verbose="--verbose" in sys.argv, force=True, trace="--trace" in sys.argv))

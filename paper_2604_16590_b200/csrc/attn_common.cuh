@@ -63,7 +63,22 @@ struct AttnParams {
   int Ab, Bb, tiles_a, num_tiles;
   // flash kernel: pairs of 128-row query tiles per group, 128-row KV tiles
   int n_qpairs, nkv;
+  // diagnostics (builds with -DTSF_TRACE only): clock64 stamps of CTA 0
+  unsigned long long* trace;
 };
+
+#ifdef TSF_TRACE
+constexpr int TRACE_PER_WARP = 1024;
+#define TSF_STAMP(p, w, k)                                                        \
+  do {                                                                           \
+    if ((p).trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (k) < TRACE_PER_WARP) \
+      (p).trace[(w) * TRACE_PER_WARP + (k)] = clock64();                         \
+  } while (0)
+#else
+#define TSF_STAMP(p, w, k) \
+  do {                     \
+  } while (0)
+#endif
 
 // ---- 16-bit pairs ----
 template <bool F16>

@@ -230,10 +230,12 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
           mbar_wait(&p_full[2 * t + (i & 1)], (i >> 1) & 1);
+          TSF_STAMP(p, 9, 4 * i + 2 * t);
           tc_fence_after();
           issue_pv(t, i);
           if (t == 1 && last_of_tile) mma_commit(&kv_empty[j % NST]);  // K_j/V_j free once retired
           if (more) issue_s(t, i + 2);   // reuses buffer i % 2 after PV_t(i) (in-order pipe)
+          TSF_STAMP(p, 9, 4 * i + 2 * t + 1);
         }
       }
     }
@@ -252,12 +254,15 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
 
     for (int i = 0; i < nsub; ++i) {
       const uint32_t tSb = tSrow + 64 * (i & 1);
+      TSF_STAMP(p, warp, 6 * i + 0);
       mbar_wait(&s_full[2 * t + (i & 1)], (i >> 1) & 1);
+      TSF_STAMP(p, warp, 6 * i + 1);
       tc_fence_after();
       uint32_t sv[64];
       tmem_ld_x32(tSb, sv);
       tmem_ld_x32(tSb + 32, sv + 32);
       tmem_wait_ld();
+      TSF_STAMP(p, warp, 6 * i + 2);
       const int valid = L - i * 64;  // columns >= valid are beyond the sequence
       if (valid < 64) {
 #pragma unroll
@@ -272,6 +277,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           m4[q] = max3(m4[q], __uint_as_float(sv[c + 2 * q]), __uint_as_float(sv[c + 2 * q + 1]));
       const float mx = max3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
       const float m_new = fmaxf(m_run, mx * sl2);
+      TSF_STAMP(p, warp, 6 * i + 3);
       if (i == 0) {
         m_run = m_new;
       } else {
@@ -332,10 +338,12 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         tmem_st_x16(tSb + 32 + c0 / 2, pk);
       }
       l_run += lsum;
+      TSF_STAMP(p, warp, 6 * i + 4);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[2 * t + (i & 1)]);
+      TSF_STAMP(p, warp, 6 * i + 5);
     }
 
     // ---- epilogue ----

@@ -42,6 +42,7 @@ struct tsf_handle {
   bool timing = false;
   std::vector<StageRec> recs;
   std::vector<cudaEvent_t> event_pool;
+  unsigned long long* trace = nullptr;  // TSF_TRACE builds only
 };
 
 static thread_local std::string g_create_err;
@@ -258,6 +259,13 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
   p.o = o;
   p.y = y;
+#ifdef TSF_TRACE
+  if (!h->trace) {
+    cudaMalloc(&h->trace, 16 * TRACE_PER_WARP * sizeof(unsigned long long));
+    cudaMemset(h->trace, 0, 16 * TRACE_PER_WARP * sizeof(unsigned long long));
+  }
+  p.trace = h->trace;
+#endif
   const bool f16 = (epi == EPI_BLOCK_S);  // X_t lives in fp16; x (BLOCK_T) arrives bf16
   const bool packed = v.L <= 128;
   int win = 128;
@@ -429,6 +437,7 @@ void tsf_destroy(tsf_handle* h) {
   for (auto& r : h->recs) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); }
   for (auto e : h->event_pool) cudaEventDestroy(e);
   free_workspace(h);
+  if (h->trace) cudaFree(h->trace);
   delete h;
 }
 
@@ -618,6 +627,19 @@ tsf_status tsf_reshard(tsf_handle* h, int dir, const tsf_bf16* in, tsf_bf16* out
   tm.done();
   return TSF_OK;
 }
+
+#ifdef TSF_TRACE
+// Diagnostics only (not in tsf.h): copy the clock64 stamps of CTA 0 of the last
+// traced launch (16 warps x TRACE_PER_WARP entries).
+int tsf_trace_read(tsf_handle* h, unsigned long long* host, int n) {
+  if (!h || !h->trace) return -1;
+  const int cap = 16 * TRACE_PER_WARP;
+  if (n > cap) n = cap;
+  cudaMemcpy(host, h->trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaMemset(h->trace, 0, cap * sizeof(unsigned long long));
+  return n;
+}
+#endif
 
 tsf_status tsf_transpose(tsf_handle* h, int A, int B, const tsf_bf16* in, tsf_bf16* out, void* stream) {
   if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");

@@ -1,0 +1,64 @@
+"""Timeline of CTA 0 of the flash kernel from clock64 stamps (diagnostics).
+
+    python -m paper_2604_16590_b200.build --trace
+    TSF_LIB=paper_2604_16590_b200/libtsf_trace.so python tools/trace_flash.py [K N H d]
+
+Softmax warp stamps per sub-step i: 0 loop top, 1 S ready (s_full), 2 S in
+registers, 3 row max done, 4 P stored, 5 p_full arrived.  MMA warp (9): per
+sub-step i and tile t: 4i+2t p_full seen, 4i+2t+1 PV(i) and S(i+2) issued.
+"""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np
+import torch
+
+import synth
+import paper_2604_16590_b200 as tsf
+
+PER_WARP = 1024
+
+
+def main():
+    K, N, H, d = (int(a) for a in sys.argv[1:5]) if len(sys.argv) >= 5 else (8, 4096, 16, 64)
+    layer = tsf.Layer(K, N, H, d)
+    x = synth.bits_to_torch(synth.make_iid(K, N, H, d, seed=0), "cuda")
+    for _ in range(3):
+        layer.block(x)
+    torch.cuda.synchronize()
+    L = tsf.lib()
+    buf = (ctypes.c_ulonglong * (16 * PER_WARP))()
+    L.tsf_trace_read.restype = ctypes.c_int
+    L.tsf_trace_read(layer._h, buf, 16 * PER_WARP)        # clear
+    layer.block(x)
+    torch.cuda.synchronize()
+    L.tsf_trace_read(layer._h, buf, 16 * PER_WARP)
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(16, PER_WARP).astype(np.int64)
+    nsub = (N + 63) // 64
+    t0 = a[a > 0].min()
+    print(f"nsub={nsub}  kernel span (CTA0 stamps) {a.max() - t0} cycles")
+    phases = ["wait S", "ld S", "max", "exp+st", "arrive", "to next"]
+    for w in range(8):
+        s = a[w, :6 * nsub].reshape(nsub, 6)
+        dif = np.diff(s, axis=1)
+        nxt = s[1:, 0] - s[:-1, 5]
+        per = dif.mean(0).tolist() + [nxt.mean()]
+        tot = (s[-1, 5] - s[0, 0]) / nsub
+        print(f"warp {w}: cycles/sub-step {tot:7.1f} | " + " ".join(f"{p} {v:6.1f}" for p, v in zip(phases, per)))
+    m = a[9, :4 * nsub].reshape(nsub, 4)
+    print("MMA warp: mean cycles p_full0->issued0 %.1f, issued0->p_full1 %.1f, p_full1->issued1 %.1f, "
+          "issued1->next p_full0 %.1f" % (np.diff(m, axis=1).mean(0)[0], np.diff(m, axis=1).mean(0)[1],
+                                          np.diff(m, axis=1).mean(0)[2], (m[1:, 0] - m[:-1, 3]).mean()))
+    print("first sub-steps, warp 0 and warp 4 (relative to kernel start):")
+    for i in range(min(6, nsub)):
+        print(i, (a[0, 6 * i:6 * i + 6] - t0).tolist(), (a[4, 6 * i:6 * i + 6] - t0).tolist(),
+              (a[9, 4 * i:4 * i + 4] - t0).tolist())
+    os.makedirs("gpurun_out", exist_ok=True)
+    np.save("gpurun_out/trace_flash.npy", a)
+
+
+if __name__ == "__main__":
+    main()
