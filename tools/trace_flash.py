@@ -24,22 +24,24 @@ PER_WARP = 1024
 
 def main():
     K, N, H, d = (int(a) for a in sys.argv[1:5]) if len(sys.argv) >= 5 else (8, 4096, 16, 64)
+    what = sys.argv[5] if len(sys.argv) >= 6 else "block"
     layer = tsf.Layer(K, N, H, d)
     x = synth.bits_to_torch(synth.make_iid(K, N, H, d, seed=0), "cuda")
+    run = (lambda: layer.block(x)) if what == "block" else (lambda: layer.spatial(x, x, x))
     for _ in range(3):
-        layer.block(x)
+        run()
     torch.cuda.synchronize()
     L = tsf.lib()
     buf = (ctypes.c_ulonglong * (16 * PER_WARP))()
     L.tsf_trace_read.restype = ctypes.c_int
     L.tsf_trace_read(layer._h, buf, 16 * PER_WARP)        # clear
-    layer.block(x)
+    run()
     torch.cuda.synchronize()
     L.tsf_trace_read(layer._h, buf, 16 * PER_WARP)
     a = np.frombuffer(buf, dtype=np.uint64).reshape(16, PER_WARP).astype(np.int64)
     nsub = (N + 63) // 64
     t0 = a[a > 0].min()
-    print(f"nsub={nsub}  kernel span (CTA0 stamps) {a.max() - t0} cycles")
+    print(f"{what} TSF_EMU={os.environ.get('TSF_EMU', 'default')} nsub={nsub}  kernel span (CTA0 stamps) {a.max() - t0} cycles")
     phases = ["wait S", "ld S", "max", "exp+st", "arrive", "to next"]
     for w in range(8):
         s = a[w, :6 * nsub].reshape(nsub, 6)
