@@ -31,10 +31,11 @@
 // half of tensor peak (16 ex2/clk/SM vs 4d MMA flops per score).
 //
 // Warp roles (384 threads): warps 0-3 softmax of tile 0, warps 4-7 softmax of
-// tile 1 (thread owns TMEM lane = tile row), warp 8 TMA producer, warp 9 MMA
-// issuer and TMEM owner, warps 10-11 convert bf16 tiles to fp16 in the block's
-// temporal stage (otherwise idle; they complete the third warpgroup so
-// setmaxnreg can move registers to the softmax warpgroups).  In the block
+// tile 1 (thread owns TMEM lane = tile row), warp 8 TMA producer, warps 9 and
+// 10 MMA issuers of tile 0 and tile 1 (independent, so one tile's issue never
+// waits for the other tile's softmax; warp 9 owns TMEM), warp 11 converts bf16
+// tiles to fp16 in the block's temporal stage (otherwise idle; it completes
+// the third warpgroup so setmaxnreg can move registers to the softmax warps).  In the block
 // modes q = k = v, so one TMA tile per stage serves as K (K-major view for
 // QK^T) and V (MN-major view for PV).
 #pragma once
@@ -110,10 +111,10 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     for (int s = 0; s < NST; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
-      mbar_init(&kv_conv[s], 2);
+      mbar_init(&kv_empty[s], 2);  // one commit from each tile's MMA issuer
+      mbar_init(&kv_conv[s], 1);
     }
-    mbar_init(q_conv, 2);
+    mbar_init(q_conv, 1);
     for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
@@ -163,9 +164,10 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       }
     }
     __syncwarp();
-  } else if (warp == 9) {
-    // ===================== MMA issuer =====================
+  } else if (warp == 9 || warp == 10) {
+    // ===================== MMA issuers: warp 9 -> tile 0, warp 10 -> tile 1 =====================
     reg_dealloc<56>();
+    const int t = warp - 9;
     if (elect_one()) {
       constexpr uint32_t idesc_qk = make_idesc(128, 64, 0, 0, F16);
       constexpr uint32_t idesc_pv = make_idesc(128, D, 0, 1, F16);
@@ -215,28 +217,21 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       else mbar_wait(q_full, 0);
       wait_k(0);
       tc_fence_after();
-      issue_s(0, 0);
-      issue_s(1, 0);
-      if (nsub > 1) {
-        issue_s(0, 1);
-        issue_s(1, 1);
-      }
+      issue_s(t, 0);
+      if (nsub > 1) issue_s(t, 1);
       for (int i = 0; i < nsub; ++i) {
         const int j = i >> 1;
         if ((i & 1) == 0) wait_v(j);
         const bool last_of_tile = (i & 1) || i == nsub - 1;
         const bool more = i + 2 < nsub;
         if (more && ((i + 2) & 1) == 0) wait_k((i + 2) >> 1);
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          mbar_wait(&p_full[2 * t + (i & 1)], (i >> 1) & 1);
-          TSF_STAMP(p, 9, 4 * i + 2 * t);
-          tc_fence_after();
-          issue_pv(t, i);
-          if (t == 1 && last_of_tile) mma_commit(&kv_empty[j % NST]);  // K_j/V_j free once retired
-          if (more) issue_s(t, i + 2);   // reuses buffer i % 2 after PV_t(i) (in-order pipe)
-          TSF_STAMP(p, 9, 4 * i + 2 * t + 1);
-        }
+        mbar_wait(&p_full[2 * t + (i & 1)], (i >> 1) & 1);
+        TSF_STAMP(p, warp, 2 * i);
+        tc_fence_after();
+        issue_pv(t, i);
+        if (last_of_tile) mma_commit(&kv_empty[j % NST]);  // K_j/V_j free once both tiles' MMAs retire
+        if (more) issue_s(t, i + 2);   // reuses buffer i % 2 after PV_t(i) (same issuer: in order)
+        TSF_STAMP(p, warp, 2 * i + 1);
       }
     }
     __syncwarp();
@@ -366,16 +361,16 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       epilogue_row<D, 128, EPI>(p, o, 1.0f / l_run, off, sQ + t * C::TILE_BYTES, row);
     }
   } else {
-    // ===================== converter warps 10-11 (block temporal stage) =====================
+    // ===================== converter warp 11 (block temporal stage) =====================
     reg_dealloc<56>();
     if constexpr (CONVERT) {
       // bf16 tiles from TMA -> fp16 in place (rows are whole 16-byte units, so
-      // the swizzle does not matter); 64 threads, one row-chunk unit at a time
+      // the swizzle does not matter); 32 threads, one row-chunk unit at a time
       constexpr int UPR = 2 * D / 16;  // 16-byte units per row
       constexpr int UPC = C::SWB / 16;
-      const uint32_t ct = threadIdx.x - 320;
+      const uint32_t ct = threadIdx.x - 352;
       auto convert_tile = [&](uint8_t* tile) {
-        for (uint32_t i = ct; i < 128 * UPR; i += 64) {
+        for (uint32_t i = ct; i < 128 * UPR; i += 32) {
           const uint32_t row = i / UPR, u = i % UPR;
           cvt_unit_bf16_to_f16(tile + (u / UPC) * C::CHUNK_BYTES + row * C::SWB + (u % UPC) * 16);
         }

@@ -50,14 +50,14 @@ def main():
         per = dif.mean(0).tolist() + [nxt.mean()]
         tot = (s[-1, 5] - s[0, 0]) / nsub
         print(f"warp {w}: cycles/sub-step {tot:7.1f} | " + " ".join(f"{p} {v:6.1f}" for p, v in zip(phases, per)))
-    m = a[9, :4 * nsub].reshape(nsub, 4)
-    print("MMA warp: mean cycles p_full0->issued0 %.1f, issued0->p_full1 %.1f, p_full1->issued1 %.1f, "
-          "issued1->next p_full0 %.1f" % (np.diff(m, axis=1).mean(0)[0], np.diff(m, axis=1).mean(0)[1],
-                                          np.diff(m, axis=1).mean(0)[2], (m[1:, 0] - m[:-1, 3]).mean()))
+    for w in (9, 10):
+        m = a[w, :2 * nsub].reshape(nsub, 2)
+        print(f"MMA warp {w}: mean cycles p_full->issued {np.diff(m, axis=1).mean():.1f}, "
+              f"issued->next p_full {(m[1:, 0] - m[:-1, 1]).mean():.1f}")
     print("first sub-steps, warp 0 and warp 4 (relative to kernel start):")
     for i in range(min(6, nsub)):
         print(i, (a[0, 6 * i:6 * i + 6] - t0).tolist(), (a[4, 6 * i:6 * i + 6] - t0).tolist(),
-              (a[9, 4 * i:4 * i + 4] - t0).tolist())
+              (a[9, 2 * i:2 * i + 2] - t0).tolist(), (a[10, 2 * i:2 * i + 2] - t0).tolist())
     os.makedirs("gpurun_out", exist_ok=True)
     np.save("gpurun_out/trace_flash.npy", a)
 
