@@ -247,35 +247,32 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     float m_run = -INFINITY;  // running max, log2-scaled units
     float l_run = 0.f;        // used when !ONES
 
-    // Software-pipelined over sub-steps: while the exponentials of S(i) run
-    // (MUFU / FMA pipes) the row max of S(i+1) (ALU) is computed, so S(i+1)'s
-    // wait, TMEM load and max are off the critical path.
-    auto load_s = [&](int i, uint32_t* sv) {
-      mbar_wait(&s_full[2 * t + (i & 1)], (i >> 1) & 1);
-      tc_fence_after();
+    for (int i = 0; i < nsub; ++i) {
       const uint32_t tSb = tSrow + 64 * (i & 1);
+      TSF_STAMP(p, warp, 6 * i + 0);
+      mbar_wait(&s_full[2 * t + (i & 1)], (i >> 1) & 1);
+      TSF_STAMP(p, warp, 6 * i + 1);
+      tc_fence_after();
+      uint32_t sv[64];
       tmem_ld_x32(tSb, sv);
       tmem_ld_x32(tSb + 32, sv + 32);
       tmem_wait_ld();
+      TSF_STAMP(p, warp, 6 * i + 2);
       const int valid = L - i * 64;  // columns >= valid are beyond the sequence
       if (valid < 64) {
 #pragma unroll
         for (int c = 0; c < 64; ++c) sv[c] = (c < valid) ? sv[c] : 0xFF800000u;  // -inf
       }
-    };
-    auto row_max = [&](const uint32_t* sv) {  // 4 independent FMNMX3 chains
+      // row max: 4 independent FMNMX3 chains
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
       for (int c = 0; c < 64; c += 8)
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           m4[q] = max3(m4[q], __uint_as_float(sv[c + 2 * q]), __uint_as_float(sv[c + 2 * q + 1]));
-      return max3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
-    };
-    float mx = 0.f;  // row max (raw score units) of the sub-step about to be processed
-    auto step = [&](int i, const uint32_t* sv, uint32_t* sv_next) {
-      TSF_STAMP(p, warp, 6 * i + 0);
+      const float mx = max3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
       const float m_new = fmaxf(m_run, mx * sl2);
+      TSF_STAMP(p, warp, 6 * i + 3);
       if (i == 0) {
         m_run = m_new;
       } else {
@@ -307,10 +304,6 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           }
         }
       }
-      TSF_STAMP(p, warp, 6 * i + 1);
-      if (i + 1 < nsub) load_s(i + 1, sv_next);
-      TSF_STAMP(p, warp, 6 * i + 2);
-      const uint32_t tSb = tSrow + 64 * (i & 1);
       const float nmb = -m_run;
       float lsum = 0.f;
 #pragma unroll
@@ -324,8 +317,8 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
             ex2_poly2(p0, p1, x0, x1);   // FMA/ALU pipes
             pk[(c - c0) / 2] = pack2<F16>(p0, p1);
           } else if constexpr (F16) {
-            // fp16 P: exponent of the packed fp16 pair (x <= RESCALE_LOG2 so
-            // 2^x <= 256 fits fp16)
+            // fp16 P: exponent of the packed fp16 pair, one MUFU op per two
+            // scores (x <= RESCALE_LOG2 so 2^x <= 256 fits fp16)
             pk[(c - c0) / 2] = ex2_f16x2(pack2<true>(x0, x1));
           } else {
             p0 = ex2(x0);                // MUFU
@@ -339,7 +332,6 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         }
         tmem_st_x16(tSb + 32 + c0 / 2, pk);
       }
-      const float mx_next = row_max(sv_next);  // ALU work overlapping the exponentials
       l_run += lsum;
       TSF_STAMP(p, warp, 6 * i + 4);
       tmem_wait_st();
@@ -347,15 +339,6 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[2 * t + (i & 1)]);
       TSF_STAMP(p, warp, 6 * i + 5);
-      mx = mx_next;
-    };
-
-    uint32_t sa[64], sb[64];
-    load_s(0, sa);
-    mx = row_max(sa);
-    for (int i = 0; i < nsub; i += 2) {
-      step(i, sa, sb);
-      if (i + 1 < nsub) step(i + 1, sb, sa);
     }
 
     // ---- epilogue ----

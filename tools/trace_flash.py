@@ -42,10 +42,9 @@ def main():
     nsub = (N + 63) // 64
     t0 = a[a > 0].min()
     print(f"{what} TSF_EMU={os.environ.get('TSF_EMU', 'default')} nsub={nsub}  kernel span (CTA0 stamps) {a.max() - t0} cycles")
-    phases = ["rescale chk", "wait+ld S(i+1)", "-", "exp+max", "arrive", "to next"]
+    phases = ["wait S", "ld S", "max", "exp+st", "arrive", "to next"]
     for w in range(8):
-        s = a[w, :6 * nsub].reshape(nsub, 6).copy()
-        s[:, 3] = s[:, 2]
+        s = a[w, :6 * nsub].reshape(nsub, 6)
         dif = np.diff(s, axis=1)
         nxt = s[1:, 0] - s[:-1, 5]
         per = dif.mean(0).tolist() + [nxt.mean()]
