@@ -45,6 +45,7 @@
 namespace tsf {
 
 constexpr float RESCALE_LOG2 = 8.0f;
+constexpr bool PINGPONG = true;
 
 template <int D, int EPI, int NST>
 struct FlashCfg {
@@ -304,6 +305,9 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           }
         }
       }
+      // ping-pong: the two warpgroups take turns for the exponential phase
+      // (MUFU-bound), so one's exps overlap the other's waits / max / stores
+      if (PINGPONG && !(t == 0 && i == 0)) named_bar_sync(1 + t, 256);
       const float nmb = -m_run;
       float lsum = 0.f;
 #pragma unroll
@@ -332,6 +336,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         }
         tmem_st_x16(tSb + 32 + c0 / 2, pk);
       }
+      if (PINGPONG) named_bar_arrive(2 - t, 256);
       l_run += lsum;
       TSF_STAMP(p, warp, 6 * i + 4);
       tmem_wait_st();
@@ -341,6 +346,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       TSF_STAMP(p, warp, 6 * i + 5);
     }
 
+    if (PINGPONG && t == 0) named_bar_sync(1, 256);  // consume warpgroup 1's last turn
     // ---- epilogue ----
     mbar_wait(&o_done[t], 0);
     tc_fence_after();
