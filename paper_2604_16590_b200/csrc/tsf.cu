@@ -192,9 +192,9 @@ static tsf_status launch_flash_emu(tsf_handle* h, cudaStream_t st, const CUtenso
 }
 
 // exp2 emulation share (of 16) for the d = 64 flash kernel: TSF_EMU overrides
-// the default for experiments.  bf16 P (standalone calls) uses fp32 MUFU ex2,
-// where 6/16 on the FMA pipe measured best; fp16 P (block) uses the packed
-// f16x2 MUFU ex2 (two scores per op) and needs no emulation.
+// the default for experiments.  (ex2.approx.f16x2 lowers to two scalar
+// MUFU.EX2.F16 + PRMT on sm_100a, so fp16 P gains nothing from it; both
+// precisions use fp32 MUFU ex2 with part of the exps on the FMA pipe.)
 static int emu_setting(int d, int epi) {
   static int env = -2;
   if (env == -2) {
@@ -203,7 +203,7 @@ static int emu_setting(int d, int epi) {
   }
   if (d != 64) return 0;
   if (env >= 0) return env;
-  return epi == EPI_OUT16 ? 6 : 0;
+  return epi == EPI_OUT16 ? 6 : 4;
 }
 
 template <int D, int EPI>
