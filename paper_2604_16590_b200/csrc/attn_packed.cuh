@@ -165,22 +165,26 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
     const int gi = g, li = (int)r - g * L;
     const float sl2 = p.scale_log2;
 
+    // x tile (bf16 from TMA) -> fp16 in place, each thread its own row; done
+    // for tile i+1 before the epilogue of tile i so the MMA of i+1 overlaps it
+    auto convert = [&](int i) {
+      const int s = i % NST;
+      mbar_wait(&full[s], (i / NST) & 1);
+      uint8_t* tile = smem + s * C::STAGE_BYTES;
+#pragma unroll
+      for (int u = 0; u < D / 8; ++u) {
+        constexpr int UPC = C::SWB / 16;
+        cvt_unit_bf16_to_f16(tile + (u / UPC) * C::CHUNK_BYTES + (r * C::SWB) + (u % UPC) * 16);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(conv_full);
+    };
+    if (CONVERT && my_tiles > 0) convert(0);
+
     for (int i = 0; i < my_tiles; ++i) {
       const int tile = blockIdx.x + i * gridDim.x;
       const int s = i % NST;
-      if constexpr (CONVERT) {
-        // x tile (bf16 from TMA) -> fp16 in place: each thread converts its row
-        mbar_wait(&full[s], (i / NST) & 1);
-        uint8_t* tile = smem + s * C::STAGE_BYTES;
-#pragma unroll
-        for (int u = 0; u < D / 8; ++u) {
-          constexpr int UPC = C::SWB / 16;
-          cvt_unit_bf16_to_f16(tile + (u / UPC) * C::CHUNK_BYTES + (r * C::SWB) + (u % UPC) * 16);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(conv_full);
-      }
       mbar_wait(s_full, i & 1);
       tc_fence_after();
       uint32_t sv[WIN];
@@ -213,6 +217,8 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
+
+      if (CONVERT && i + 1 < my_tiles) convert(i + 1);
 
       // ---- epilogue ----
       mbar_wait(o_full, i & 1);
