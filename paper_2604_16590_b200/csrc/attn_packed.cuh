@@ -98,6 +98,7 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
         if (i >= NST) mbar_wait(&empty[s], ((i / NST) - 1) & 1);
         const int a0 = (tile % p.tiles_a) * p.Ab, b0 = (tile / p.tiles_a) * p.Bb;
         uint8_t* st = smem + s * C::STAGE_BYTES;
+        TSF_STAMP(p, 16 + 4, 2 * i);
         mbar_arrive_expect_tx(&full[s], box_bytes * C::NCH * C::NT);
 #pragma unroll
         for (int c = 0; c < C::NCH; ++c) {
@@ -131,6 +132,7 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
                  make_sdesc(ka + off, 16, 8 * C::SWB, C::SWB == 128 ? SWZ_128B : SWZ_64B), idesc_qk, k > 0);
         }
         mma_commit(s_full);
+        TSF_STAMP(p, 16 + 5, 4 * i);
         mbar_wait(p_full, i & 1);
         tc_fence_after();
         if (i > 0) { mbar_wait(o_empty, (i - 1) & 1); tc_fence_after(); }
@@ -142,6 +144,7 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
                  idesc_pv, k > 0);
         }
         mma_commit(o_full);
+        TSF_STAMP(p, 16 + 5, 4 * i + 1);
       }
     }
     __syncwarp();
@@ -185,7 +188,9 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
     for (int i = 0; i < my_tiles; ++i) {
       const int tile = blockIdx.x + i * gridDim.x;
       const int s = i % NST;
+      TSF_STAMP(p, 16 + warp, 6 * i + 0);
       mbar_wait(s_full, i & 1);
+      TSF_STAMP(p, 16 + warp, 6 * i + 1);
       tc_fence_after();
       uint32_t sv[WIN];
 #pragma unroll
@@ -217,11 +222,14 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
+      TSF_STAMP(p, 16 + warp, 6 * i + 2);
 
       if (CONVERT && i + 1 < my_tiles) convert(i + 1);
+      TSF_STAMP(p, 16 + warp, 6 * i + 3);
 
       // ---- epilogue ----
       mbar_wait(o_full, i & 1);
+      TSF_STAMP(p, 16 + warp, 6 * i + 4);
       tc_fence_after();
       float o[D];
 #pragma unroll
@@ -239,6 +247,7 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      TSF_STAMP(p, 16 + warp, 6 * i + 5);
     }
   }
 

@@ -261,8 +261,8 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
   p.y = y;
 #ifdef TSF_TRACE
   if (!h->trace) {
-    cudaMalloc(&h->trace, 16 * TRACE_PER_WARP * sizeof(unsigned long long));
-    cudaMemset(h->trace, 0, 16 * TRACE_PER_WARP * sizeof(unsigned long long));
+    cudaMalloc(&h->trace, 32 * TRACE_PER_WARP * sizeof(unsigned long long));
+    cudaMemset(h->trace, 0, 32 * TRACE_PER_WARP * sizeof(unsigned long long));
   }
   p.trace = h->trace;
 #endif
@@ -633,7 +633,7 @@ tsf_status tsf_reshard(tsf_handle* h, int dir, const tsf_bf16* in, tsf_bf16* out
 // traced launch (16 warps x TRACE_PER_WARP entries).
 int tsf_trace_read(tsf_handle* h, unsigned long long* host, int n) {
   if (!h || !h->trace) return -1;
-  const int cap = 16 * TRACE_PER_WARP;
+  const int cap = 32 * TRACE_PER_WARP;
   if (n > cap) n = cap;
   cudaMemcpy(host, h->trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   cudaMemset(h->trace, 0, cap * sizeof(unsigned long long));
