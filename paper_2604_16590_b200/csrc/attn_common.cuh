@@ -159,4 +159,36 @@ __device__ __forceinline__ void epilogue_row(const AttnParams& p, const float* o
   }
 }
 
+// Epilogue for one row written back IN PLACE into its swizzled shared-memory
+// row (the tile the row's input came from), for a TMA store of the whole tile.
+// EPI_OUT16: bf16(O/l); EPI_BLOCK_T: fp16(x + O/l) with x read from the same row.
+template <int D, int ROWS, int EPI>
+__device__ __forceinline__ void epilogue_row_smem(const float* o_acc, float inv_l, uint8_t* tile, uint32_t r) {
+  constexpr int SWB = (2 * D < 128) ? 2 * D : 128;
+  constexpr int UPC = SWB / 16;
+#pragma unroll
+  for (int u = 0; u < D / 8; ++u) {
+    uint4* ptr = reinterpret_cast<uint4*>(tile + (u / UPC) * (ROWS * SWB) + swz_off<SWB>(r, u % UPC));
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = o_acc[8 * u + i] * inv_l;
+    uint4 w;
+    if constexpr (EPI == EPI_OUT16) {
+      w.x = pack2<false>(v[0], v[1]);
+      w.y = pack2<false>(v[2], v[3]);
+      w.z = pack2<false>(v[4], v[5]);
+      w.w = pack2<false>(v[6], v[7]);
+    } else {
+      const uint4 rr = *ptr;
+      const float2 x0 = unpack2<true>(rr.x), x1 = unpack2<true>(rr.y), x2 = unpack2<true>(rr.z),
+                   x3 = unpack2<true>(rr.w);
+      w.x = pack2<true>(x0.x + v[0], x0.y + v[1]);
+      w.y = pack2<true>(x1.x + v[2], x1.y + v[3]);
+      w.z = pack2<true>(x2.x + v[4], x2.y + v[5]);
+      w.w = pack2<true>(x3.x + v[6], x3.y + v[7]);
+    }
+    *ptr = w;
+  }
+}
+
 }  // namespace tsf

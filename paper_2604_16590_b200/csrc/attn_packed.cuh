@@ -36,10 +36,15 @@ struct PackedCfg {
 template <int D, int WIN, int EPI, bool SHARED, int NST>
 __global__ void __launch_bounds__(192, (192 + D <= 256) ? 2 : 1)
 attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
-                   const __grid_constant__ CUtensorMap tv, const AttnParams p) {
+                   const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap to,
+                   const AttnParams p) {
   using C = PackedCfg<D, WIN, EPI, SHARED, NST>;
   constexpr bool F16 = EpiTraits<EPI>::F16;
   constexpr bool CONVERT = EpiTraits<EPI>::CONVERT;
+  // 16-bit outputs go through shared memory and one TMA store per tile (rows of
+  // a tile are scattered in HBM: per-thread row stores touch 32 lines per
+  // instruction); the fp32 y of EPI_BLOCK_S is stored per thread.
+  constexpr bool TMA_OUT = (EPI != EPI_BLOCK_S);
   static_assert(SHARED == EpiTraits<EPI>::SHARED, "q = k = v exactly in the block modes");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -67,7 +72,7 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 4);
+      mbar_init(&empty[s], 1);
     }
     mbar_init(s_full, 1);
     mbar_init(p_full, 4);
@@ -91,6 +96,7 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
     if (elect_one()) {
       tma_prefetch_desc(&tq);
       if (!SHARED) { tma_prefetch_desc(&tk); tma_prefetch_desc(&tv); }
+      if (TMA_OUT) tma_prefetch_desc(&to);
       const uint32_t box_bytes = (uint32_t)(C::CH * 2) * (uint32_t)rows_used;
       for (int i = 0; i < my_tiles; ++i) {
         const int tile = blockIdx.x + i * gridDim.x;
@@ -174,10 +180,14 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
       const int s = i % NST;
       mbar_wait(&full[s], (i / NST) & 1);
       uint8_t* tile = smem + s * C::STAGE_BYTES;
+      // the warp converts its own 32 rows; consecutive lanes take consecutive
+      // 16-byte units of a row (bank-conflict free)
+      constexpr int UPR = D / 8, UPC = C::SWB / 16;
 #pragma unroll
-      for (int u = 0; u < D / 8; ++u) {
-        constexpr int UPC = C::SWB / 16;
-        cvt_unit_bf16_to_f16(tile + (u / UPC) * C::CHUNK_BYTES + (r * C::SWB) + (u % UPC) * 16);
+      for (int k = 0; k < UPR; ++k) {
+        const uint32_t idx = lane + 32 * k;
+        const uint32_t row = warp * 32 + idx / UPR, u = idx % UPR;
+        cvt_unit_bf16_to_f16(tile + (u / UPC) * C::CHUNK_BYTES + row * C::SWB + (u % UPC) * 16);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
@@ -239,18 +249,34 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
       __syncwarp();
       if (lane == 0) mbar_arrive(o_empty);
 
-      const int a = (tile % p.tiles_a) * p.Ab + gi % p.Ab;
-      const int b = (tile / p.tiles_a) * p.Bb + gi / p.Ab;
-      if (row_ok && b < p.B && l > 0.f) {
-        const long long off = (long long)li * p.sL + (long long)a * p.sA + (long long)b * p.sB;
-        epilogue_row<D, 128, EPI>(p, o, 1.0f / l, off, smem + s * C::STAGE_BYTES, r);
+      const int a0 = (tile % p.tiles_a) * p.Ab, b0 = (tile / p.tiles_a) * p.Bb;
+      if constexpr (TMA_OUT) {
+        // rows into the stage's (first) tile in place, then one TMA store
+        if (row_ok) epilogue_row_smem<D, 128, EPI>(o, 1.0f / l, smem + s * C::STAGE_BYTES, r);
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (threadIdx.x == 0) {
+#pragma unroll
+          for (int c = 0; c < C::NCH; ++c)
+            tma_store_4d(&to, smem + s * C::STAGE_BYTES + c * C::CHUNK_BYTES, c * C::CH, 0, a0, b0);
+          bulk_commit();
+          bulk_wait_read0();          // stage may be refilled once the store has read it
+          mbar_arrive(&empty[s]);
+        }
+      } else {
+        const int a = a0 + gi % p.Ab, b = b0 + gi / p.Ab;
+        if (row_ok && b < p.B && l > 0.f) {
+          const long long off = (long long)li * p.sL + (long long)a * p.sA + (long long)b * p.sB;
+          epilogue_row<D, 128, EPI>(p, o, 1.0f / l, off, smem + s * C::STAGE_BYTES, r);
+        }
+        named_bar_sync(1, 128);
+        if (threadIdx.x == 0) mbar_arrive(&empty[s]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
       TSF_STAMP(p, 16 + warp, 6 * i + 5);
     }
   }
 
+  if (TMA_OUT && threadIdx.x == 0) bulk_wait0();  // all output stores complete
   tc_fence_before();
   __syncthreads();
   if (warp == 4) {

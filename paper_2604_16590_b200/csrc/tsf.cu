@@ -157,12 +157,12 @@ struct StageTimer {
 // ---------------------------------------------------------------------------
 // kernel launch
 // ---------------------------------------------------------------------------
-template <typename KernelT>
+template <typename KernelT, typename... Maps>
 static tsf_status launch(tsf_handle* h, KernelT kern, int grid, int threads, int smem, cudaStream_t st,
-                         const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const AttnParams& p) {
+                         const AttnParams& p, const Maps&... maps) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return fail(h, TSF_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-  kern<<<grid, threads, smem, st>>>(mq, mk, mv, p);
+  kern<<<grid, threads, smem, st>>>(maps..., p);
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, TSF_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
   h->launches++;
@@ -171,13 +171,13 @@ static tsf_status launch(tsf_handle* h, KernelT kern, int grid, int threads, int
 
 template <int D, int WIN, int EPI, bool SHARED>
 static tsf_status launch_packed_t(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
-                                  const CUtensorMap& mv, const AttnParams& p) {
+                                  const CUtensorMap& mv, const CUtensorMap& mo, const AttnParams& p) {
   constexpr int NST = SHARED ? 4 : 2;
   using C = PackedCfg<D, WIN, EPI, SHARED, NST>;
   const int per_sm = (C::TCOLS == 256 && 2 * C::SMEM <= 227 * 1024) ? 2 : 1;
   int grid = h->num_sms * per_sm;
   if (grid > p.num_tiles) grid = p.num_tiles;
-  return launch(h, attn_packed_kernel<D, WIN, EPI, SHARED, NST>, grid, C::THREADS, C::SMEM, st, mq, mk, mv, p);
+  return launch(h, attn_packed_kernel<D, WIN, EPI, SHARED, NST>, grid, C::THREADS, C::SMEM, st, p, mq, mk, mv, mo);
 }
 
 template <int D, int EPI, int EMU>
@@ -188,7 +188,7 @@ static tsf_status launch_flash_emu(tsf_handle* h, cudaStream_t st, const CUtenso
   using C = FlashCfg<D, EPI, NST>;
   const long long grid = (long long)p.n_qpairs * p.A * p.B;
   if (grid > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "grid too large");
-  return launch(h, attn_flash_kernel<D, EPI, NST, EMU>, (int)grid, C::THREADS, C::SMEM, st, mq, mk, mv, p);
+  return launch(h, attn_flash_kernel<D, EPI, NST, EMU>, (int)grid, C::THREADS, C::SMEM, st, p, mq, mk, mv);
 }
 
 // exp2 emulation share (of 16) for the d = 64 flash kernel: TSF_EMU overrides
@@ -223,22 +223,24 @@ static tsf_status launch_flash_t(tsf_handle* h, cudaStream_t st, const CUtensorM
 
 template <int D, int EPI, bool SHARED>
 static tsf_status dispatch_packed_win(tsf_handle* h, int win, cudaStream_t st, const CUtensorMap& mq,
-                                      const CUtensorMap& mk, const CUtensorMap& mv, const AttnParams& p) {
+                                      const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mo,
+                                      const AttnParams& p) {
   switch (win) {
-    case 32: return launch_packed_t<D, 32, EPI, SHARED>(h, st, mq, mk, mv, p);
-    case 64: return launch_packed_t<D, 64, EPI, SHARED>(h, st, mq, mk, mv, p);
-    default: return launch_packed_t<D, 128, EPI, SHARED>(h, st, mq, mk, mv, p);
+    case 32: return launch_packed_t<D, 32, EPI, SHARED>(h, st, mq, mk, mv, mo, p);
+    case 64: return launch_packed_t<D, 64, EPI, SHARED>(h, st, mq, mk, mv, mo, p);
+    default: return launch_packed_t<D, 128, EPI, SHARED>(h, st, mq, mk, mv, mo, p);
   }
 }
 
 template <int D>
 static tsf_status dispatch_d(tsf_handle* h, bool packed, int win, int epi, cudaStream_t st, const CUtensorMap& mq,
-                             const CUtensorMap& mk, const CUtensorMap& mv, const AttnParams& p) {
+                             const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mo,
+                             const AttnParams& p) {
   if (packed) {
     switch (epi) {
-      case EPI_OUT16: return dispatch_packed_win<D, EPI_OUT16, false>(h, win, st, mq, mk, mv, p);
-      case EPI_BLOCK_T: return dispatch_packed_win<D, EPI_BLOCK_T, true>(h, win, st, mq, mk, mv, p);
-      default: return dispatch_packed_win<D, EPI_BLOCK_S, true>(h, win, st, mq, mk, mv, p);
+      case EPI_OUT16: return dispatch_packed_win<D, EPI_OUT16, false>(h, win, st, mq, mk, mv, mo, p);
+      case EPI_BLOCK_T: return dispatch_packed_win<D, EPI_BLOCK_T, true>(h, win, st, mq, mk, mv, mo, p);
+      default: return dispatch_packed_win<D, EPI_BLOCK_S, true>(h, win, st, mq, mk, mv, mo, p);
     }
   }
   switch (epi) {
@@ -269,7 +271,8 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
   const bool f16 = (epi == EPI_BLOCK_S);  // X_t lives in fp16; x (BLOCK_T) arrives bf16
   const bool packed = v.L <= 128;
   int win = 128;
-  CUtensorMap mq, mk, mv;
+  CUtensorMap mq, mk, mv, mo;
+  memset(&mo, 0, sizeof mo);
   tsf_status s;
   if (packed) {
     const int G = 128 / v.L;
@@ -287,6 +290,8 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
     if ((s = make_map(h, &mq, q, d, v, v.L, Ab, Bb, f16)) != TSF_OK) return s;
     if ((s = make_map(h, &mk, k, d, v, v.L, Ab, Bb, f16)) != TSF_OK) return s;
     if ((s = make_map(h, &mv, vv, d, v, v.L, Ab, Bb, f16)) != TSF_OK) return s;
+    // output map (16-bit outputs): bf16 for the standalone calls, fp16 X_t for the block
+    if (epi != EPI_BLOCK_S && (s = make_map(h, &mo, o, d, v, v.L, Ab, Bb, epi == EPI_BLOCK_T)) != TSF_OK) return s;
   } else {
     p.n_qpairs = (v.L + 255) / 256;
     p.nkv = (v.L + 127) / 128;
@@ -295,9 +300,9 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
     if ((s = make_map(h, &mv, vv, d, v, 128, 1, 1, f16)) != TSF_OK) return s;
   }
   switch (d) {
-    case 32: return dispatch_d<32>(h, packed, win, epi, st, mq, mk, mv, p);
-    case 64: return dispatch_d<64>(h, packed, win, epi, st, mq, mk, mv, p);
-    default: return dispatch_d<128>(h, packed, win, epi, st, mq, mk, mv, p);
+    case 32: return dispatch_d<32>(h, packed, win, epi, st, mq, mk, mv, mo, p);
+    case 64: return dispatch_d<64>(h, packed, win, epi, st, mq, mk, mv, mo, p);
+    default: return dispatch_d<128>(h, packed, win, epi, st, mq, mk, mv, mo, p);
   }
 }
 
