@@ -1,0 +1,76 @@
+"""Multi-GPU parity of the distributed block and reshard (run under torchrun).
+
+    torchrun --nproc-per-node P --master-addr 127.0.0.1 --master-port 29511 tools/dist_check.py [K N H d]
+
+Each rank: x token shard -> tsf_spacetime_block -> y frame shard, compared with
+the fp64 oracle on sampled rows + a full plane of the rank's frames; the
+reshard round trip must be bit-exact; y on P GPUs must equal the single-GPU
+y bitwise (same kernel tiles per group).
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+import oracle
+import synth
+import paper_2604_16590_b200 as tsf
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    K, N, H, d = (int(a) for a in sys.argv[1:5]) if len(sys.argv) >= 5 else (8 * world, 4096, 16, 64)
+    Nl, Kl = N // world, K // world
+    layer = tsf.Layer(K, N, H, d, group=dist.group.WORLD)
+    xb_full = synth.make_x(K, N, H, d, seed=0)
+    xs = synth.bits_to_torch(np.ascontiguousarray(xb_full[:, rank * Nl:(rank + 1) * Nl]), "cuda")
+    y = layer.block(xs)
+    torch.cuda.synchronize()
+
+    # parity vs the oracle on this rank's frames
+    x = synth.bf16_bits_to_f64(xb_full)
+    g = np.random.default_rng(rank)
+    rows = sorted({(int(g.integers(Kl)), int(g.integers(N)), int(g.integers(H))) for _ in range(512)})
+    want = oracle.block_rows(x, [(rank * Kl + t, n, h) for t, n, h in rows])
+    ri = torch.tensor(rows)
+    got = y[ri[:, 0], ri[:, 1], ri[:, 2]].double().cpu().numpy()
+    err = np.abs(got - want).max()
+    plane = y[0, :, 0].double().cpu().numpy()
+    perr = np.abs(plane - oracle.block_plane(x, rank * Kl, 0)).max()
+
+    # reshard round trip, bit-exact
+    fr = layer.reshard(xs, tsf.TSF_T2S)
+    back = layer.reshard(fr, tsf.TSF_S2T)
+    torch.cuda.synchronize()
+    exact_fr = torch.equal(fr.cpu(), synth.bits_to_torch(np.ascontiguousarray(xb_full[rank * Kl:(rank + 1) * Kl])))
+    exact_back = torch.equal(back, xs)
+
+    # bitwise equality with the single-GPU result (rank 0 computes the full layer)
+    same = None
+    if rank == 0:
+        single = tsf.Layer(K, N, H, d)
+        y1 = single.block(synth.bits_to_torch(xb_full, "cuda"))
+        torch.cuda.synchronize()
+        same = torch.equal(y1[:Kl], y)
+        single.close()
+    print(f"rank {rank}/{world}: block sampled max-abs {err:.3e}, plane max-abs {perr:.3e}, "
+          f"t2s exact {exact_fr}, round trip exact {exact_back}, equals single-GPU bitwise {same}", flush=True)
+    ok = err <= 2e-2 and perr <= 2e-2 and exact_fr and exact_back and (same in (None, True))
+    flag = torch.tensor([0 if ok else 1], device="cuda")
+    dist.all_reduce(flag)
+    layer.close()
+    dist.destroy_process_group()
+    if rank == 0:
+        print("DIST CHECK", "PASS" if flag.item() == 0 else "FAIL", flush=True)
+    sys.exit(0 if flag.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()
