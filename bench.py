@@ -266,10 +266,12 @@ def main():
         value = tokens * args.steps / (ms / 1e3)
         F = tsf.flops(K, N, H, d)
         # dominant kernel: the spatial flash-attention kernel; algorithmic flops
-        # per launch = 4 H d Kl N^2 (QK^T + PV) on this rank
+        # per step = 4 H d Kl N^2 (QK^T + PV) on this rank, split over the
+        # launches of a step (1, or one per head chunk when P > 1)
         n_sp = st_ms[1][1]
+        per_step = max(n_sp // args.steps, 1)
         sp_launch_ms = sp_ms / max(n_sp, 1)
-        sp_flops = 4 * H * d * Kl * N * N
+        sp_flops = 4 * H * d * Kl * N * N // per_step
         achieved = sp_flops / (sp_launch_ms / 1e3) / 1e12
         clocks = clk.summary()
         line = {
@@ -284,19 +286,22 @@ def main():
                          "frac": achieved / pk["tflops"], "traffic": traffic_from_profiles("spatial_C2"),
                          "peak_source": pk["source"] + " bf16 burst (fp16 operands: same nominal rate)",
                          "algorithmic_flops_per_launch": sp_flops, "launch_ms": sp_launch_ms,
-                         "stage_ms": {"temporal": tp_ms / max(st_ms[0][1], 1), "spatial": sp_launch_ms,
-                                      "reshard": rs_ms / max(st_ms[2][1], 1) if world > 1 else 0.0}},
+                         "launches_per_step": per_step,
+                         "stage_ms_per_step": {"temporal": tp_ms / args.steps, "spatial": sp_ms / args.steps,
+                                               "exchange (comm stream)": rs_ms / args.steps}},
             "e2e": {"value": tokens * e2e_steps / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": xh.numel() * 2, "d2h_bytes_per_step": yh.numel() * 4},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
         }
         if world > 1:
-            a2a_bytes = xs[0].numel() * 2 * (world - 1) / world
-            rs_launch_ms = rs_ms / max(st_ms[2][1], 1)
-            algbw = a2a_bytes / (rs_launch_ms / 1e3) / 1e9
-            line["a2a"] = {"bytes_sent_per_rank": a2a_bytes, "ms_incl_unpack": rs_launch_ms, "algbw_GBs": algbw,
-                           "busbw_GBs": algbw * (world - 1) / world, "nvlink_GBs_per_dir": 900}
+            a2a_bytes = xs[0].numel() * 2            # X_t (fp16) bytes per rank entering the all-to-all
+            rs_step_ms = rs_ms / args.steps
+            algbw = a2a_bytes / (rs_step_ms / 1e3) / 1e9
+            line["a2a"] = {"bytes_per_rank": a2a_bytes, "bytes_to_peers_per_rank": a2a_bytes * (world - 1) / world,
+                           "ms_per_step_comm_stream": rs_step_ms, "algbw_GBs": algbw,
+                           "busbw_GBs": algbw * (world - 1) / world, "nvlink_GBs_per_dir": 900,
+                           "overlap": "head-chunk pipeline: exchange(c+1) overlaps spatial(c)"}
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(8, N, H, d)
         print(json.dumps(line), flush=True)

@@ -55,7 +55,8 @@ __device__ __forceinline__ void cvt_unit_bf16_to_f16(uint8_t* p) {
 
 struct AttnParams {
   int L, A, B;               // sequence length, group dims
-  long long sL, sA, sB;      // element strides of the view
+  long long sL, sA, sB;      // element strides of the input view (TMA maps)
+  long long osL, osA, osB;   // element strides of the output (per-thread stores)
   float scale_log2;          // log2(e) / sqrt(d)
   void* o;                   // EPI_OUT16: bf16 output; EPI_BLOCK_T: fp16 X_t
   float* y;                  // EPI_BLOCK_S: fp32 output

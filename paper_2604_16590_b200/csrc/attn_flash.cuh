@@ -361,7 +361,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     }
     const int l_idx = qp * 256 + t * 128 + (int)row;
     if (l_idx < L) {
-      const long long off = (long long)l_idx * p.sL + (long long)ga * p.sA + (long long)gb * p.sB;
+      const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
       epilogue_row<D, 128, EPI>(p, o, 1.0f / l_run, off, sQ + t * C::TILE_BYTES, row);
     }
   } else {

@@ -266,7 +266,7 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
       } else {
         const int a = a0 + gi % p.Ab, b = b0 + gi / p.Ab;
         if (row_ok && b < p.B && l > 0.f) {
-          const long long off = (long long)li * p.sL + (long long)a * p.sA + (long long)b * p.sB;
+          const long long off = (long long)li * p.osL + (long long)a * p.osA + (long long)b * p.osB;
           epilogue_row<D, 128, EPI>(p, o, 1.0f / l, off, smem + s * C::STAGE_BYTES, r);
         }
         named_bar_sync(1, 128);

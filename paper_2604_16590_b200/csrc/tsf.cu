@@ -43,9 +43,15 @@ struct tsf_handle {
   std::vector<StageRec> recs;
   std::vector<cudaEvent_t> event_pool;
   unsigned long long* trace = nullptr;  // TSF_TRACE builds only
+  // distributed block: X_t is exchanged in nchunk head chunks on comm_stream
+  // while the spatial stage of earlier chunks runs (X_t layout [c][K][N/P][H/c][d])
+  int nchunk = 1;
+  cudaStream_t comm_stream = nullptr;
+  std::vector<cudaEvent_t> ev_t, ev_a;
 };
 
 static thread_local std::string g_create_err;
+extern "C" void tsf_destroy(tsf_handle* h);
 
 // ---------------------------------------------------------------------------
 // helpers
@@ -250,14 +256,17 @@ static tsf_status dispatch_d(tsf_handle* h, bool packed, int win, int epi, cudaS
   }
 }
 
-// Attention over one view: q/k/v (q == k == v for the block stages).
+// Attention over one view: q/k/v (q == k == v for the block stages).  The
+// output (o or y) uses the strides of `ov` (default: the input view's).
 static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, const void* k, const void* vv, int epi,
-                                void* o, float* y, cudaStream_t st) {
+                                void* o, float* y, cudaStream_t st, const View* ov = nullptr) {
+  if (!ov) ov = &v;
   const int d = h->d;
   if ((long long)v.A * v.B == 0 || v.L == 0) return TSF_OK;
   AttnParams p{};
   p.L = v.L; p.A = v.A; p.B = v.B;
   p.sL = v.sL; p.sA = v.sA; p.sB = v.sB;
+  p.osL = ov->sL; p.osA = ov->sA; p.osB = ov->sB;
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
   p.o = o;
   p.y = y;
@@ -291,7 +300,7 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
     if ((s = make_map(h, &mk, k, d, v, v.L, Ab, Bb, f16)) != TSF_OK) return s;
     if ((s = make_map(h, &mv, vv, d, v, v.L, Ab, Bb, f16)) != TSF_OK) return s;
     // output map (16-bit outputs): bf16 for the standalone calls, fp16 X_t for the block
-    if (epi != EPI_BLOCK_S && (s = make_map(h, &mo, o, d, v, v.L, Ab, Bb, epi == EPI_BLOCK_T)) != TSF_OK) return s;
+    if (epi != EPI_BLOCK_S && (s = make_map(h, &mo, o, d, *ov, v.L, Ab, Bb, epi == EPI_BLOCK_T)) != TSF_OK) return s;
   } else {
     p.n_qpairs = (v.L + 255) / 256;
     p.nkv = (v.L + 127) / 128;
@@ -426,6 +435,24 @@ tsf_status tsf_create_dist(int K, int N, int H, int d, const void* id128, int ra
       delete h;
       return fail(nullptr, TSF_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     }
+    // head chunks for the exchange / spatial overlap: TSF_NCHUNK or 2
+    int nc = 2;
+    if (const char* e = getenv("TSF_NCHUNK")) nc = atoi(e);
+    if (nc < 1) nc = 1;
+    while (nc > 1 && H % nc) --nc;
+    h->nchunk = nc;
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    if (cudaStreamCreateWithPriority(&h->comm_stream, cudaStreamNonBlocking, hi_prio) != cudaSuccess) {
+      tsf_destroy(h);
+      return fail(nullptr, TSF_ERR_CUDA, "comm stream creation failed");
+    }
+    h->ev_t.resize(nc);
+    h->ev_a.resize(nc);
+    for (int c = 0; c < nc; ++c) {
+      cudaEventCreateWithFlags(&h->ev_t[c], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&h->ev_a[c], cudaEventDisableTiming);
+    }
   }
   *out = h;
   return TSF_OK;
@@ -440,6 +467,9 @@ void tsf_destroy(tsf_handle* h) {
     else ncclCommDestroy(h->comm);
   }
   for (auto& r : h->recs) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); }
+  for (auto e : h->ev_t) cudaEventDestroy(e);
+  for (auto e : h->ev_a) cudaEventDestroy(e);
+  if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
   for (auto e : h->event_pool) cudaEventDestroy(e);
   free_workspace(h);
   if (h->trace) cudaFree(h->trace);
@@ -505,20 +535,33 @@ tsf_status tsf_spatial_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k,
   return s;
 }
 
-// X_t token shard -> frame shard: one grouped NCCL send/recv round (bytes,
-// bit-exact) and the unpack kernel.
-static tsf_status all_to_all_xt(tsf_handle* h, cudaStream_t st) {
-  const int P = h->world, Kc = h->K / P, Nc = h->N / P;
-  const size_t chunk = (size_t)Kc * Nc * h->H * h->d * 2;  // bytes per peer
+// X_t token shard -> frame shard for head chunk c: one grouped NCCL send/recv
+// round (bytes, bit-exact) on the comm stream.  Chunk c of X_t is
+// [K][N/P][Hc][d]; its frames [p K/P, (p+1) K/P) (contiguous) go to peer p;
+// the receive buffer is [P][K/P][N/P][Hc][d].
+static tsf_status exchange_chunk(tsf_handle* h, int c, cudaStream_t cs) {
+  const int P = h->world, Kc = h->K / P, Nc = h->N / P, Hc = h->H / h->nchunk;
+  const size_t chunk_elems = (size_t)h->K * Nc * Hc * h->d;
+  const size_t peer_bytes = (size_t)Kc * Nc * Hc * h->d * 2;
+  const char* src = reinterpret_cast<const char*>(h->xt + c * chunk_elems);
+  char* dst = reinterpret_cast<char*>(h->rxt + c * chunk_elems);
   TSF_NCCL(h, ncclGroupStart());
   for (int p = 0; p < P; ++p) {
-    TSF_NCCL(h, ncclSend((const char*)h->xt + p * chunk, chunk, ncclUint8, p, h->comm, st));
-    TSF_NCCL(h, ncclRecv((char*)h->rxt + p * chunk, chunk, ncclUint8, p, h->comm, st));
+    TSF_NCCL(h, ncclSend(src + p * peer_bytes, peer_bytes, ncclUint8, p, h->comm, cs));
+    TSF_NCCL(h, ncclRecv(dst + p * peer_bytes, peer_bytes, ncclUint8, p, h->comm, cs));
   }
   TSF_NCCL(h, ncclGroupEnd());
-  const int vecs = h->H * h->d * 2 / 16;
+  return TSF_OK;
+}
+
+// receive buffer [P][K/P][N/P][Hc][d] of chunk c -> frame shard [K/P][N][Hc][d]
+static tsf_status unpack_chunk(tsf_handle* h, int c, cudaStream_t st) {
+  const int P = h->world, Kc = h->K / P, Nc = h->N / P, Hc = h->H / h->nchunk;
+  const size_t chunk_elems = (size_t)h->K * Nc * Hc * h->d;
+  const int vecs = Hc * h->d * 2 / 16;
   const long long items = (long long)P * Kc * Nc * vecs;
-  reshard_perm_kernel<true><<<grid_for(h, items), 256, 0, st>>>((const uint4*)h->rxt, (uint4*)h->uxt, nullptr,
+  reshard_perm_kernel<true><<<grid_for(h, items), 256, 0, st>>>((const uint4*)(h->rxt + c * chunk_elems),
+                                                                (uint4*)(h->uxt + c * chunk_elems), nullptr,
                                                                 nullptr, P, Kc, Nc, vecs);
   TSF_CUDA(h, cudaGetLastError());
   h->launches++;
@@ -534,26 +577,55 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
   tsf_status s = check_ptrs(h, {x}, y, in_bytes, out_bytes);
   if (s != TSF_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
-  // temporal stage: X_t = x + T(x, x, x), stored fp16
-  {
+  if (P == 1) {
+    // temporal stage: X_t = x + T(x, x, x), stored fp16
+    {
+      StageTimer tm(h, st, 0);
+      s = run_attention(h, temporal_view(h->K, Nl, h->H, h->d), x, x, x, EPI_BLOCK_T, h->xt, nullptr, st);
+      tm.done();
+      if (s != TSF_OK) return s;
+    }
+    // spatial stage: y = X_t + S(X_t, X_t, X_t)
+    StageTimer tm(h, st, 1);
+    s = run_attention(h, spatial_view(Kl, h->N, h->H, h->d), h->xt, h->xt, h->xt, EPI_BLOCK_S, nullptr, y, st);
+    tm.done();
+    return s;
+  }
+  // Distributed: head-chunk pipeline.  temporal(c) for all chunks on `st`;
+  // exchange(c) on the comm stream after temporal(c); unpack(c) + spatial(c)
+  // on `st` after exchange(c), so exchange(c+1) overlaps spatial(c).
+  const int nc = h->nchunk, Hc = h->H / nc, K = h->K, N = h->N, H = h->H, d = h->d;
+  const size_t chunk_elems = (size_t)K * Nl * Hc * d;
+  for (int c = 0; c < nc; ++c) {
     StageTimer tm(h, st, 0);
-    s = run_attention(h, temporal_view(h->K, Nl, h->H, h->d), x, x, x, EPI_BLOCK_T, h->xt, nullptr, st);
+    const View vin{K, Hc, Nl, (long long)Nl * H * d, (long long)d, (long long)H * d};
+    const View vout{K, Hc, Nl, (long long)Nl * Hc * d, (long long)d, (long long)Hc * d};
+    const tsf_bf16* xc = x + (size_t)c * Hc * d;
+    s = run_attention(h, vin, xc, xc, xc, EPI_BLOCK_T, h->xt + c * chunk_elems, nullptr, st, &vout);
+    tm.done();
+    if (s != TSF_OK) return s;
+    TSF_CUDA(h, cudaEventRecord(h->ev_t[c], st));
+  }
+  for (int c = 0; c < nc; ++c) {
+    TSF_CUDA(h, cudaStreamWaitEvent(h->comm_stream, h->ev_t[c], 0));
+    StageTimer tm(h, h->comm_stream, 2);
+    s = exchange_chunk(h, c, h->comm_stream);
+    tm.done();
+    if (s != TSF_OK) return s;
+    TSF_CUDA(h, cudaEventRecord(h->ev_a[c], h->comm_stream));
+  }
+  for (int c = 0; c < nc; ++c) {
+    TSF_CUDA(h, cudaStreamWaitEvent(st, h->ev_a[c], 0));
+    if ((s = unpack_chunk(h, c, st)) != TSF_OK) return s;
+    StageTimer tm(h, st, 1);
+    const __half* u = h->uxt + c * chunk_elems;
+    const View vs{N, Hc, Kl, (long long)Hc * d, (long long)d, (long long)N * Hc * d};
+    const View vy{N, Hc, Kl, (long long)H * d, (long long)d, (long long)N * H * d};
+    s = run_attention(h, vs, u, u, u, EPI_BLOCK_S, nullptr, y + (size_t)c * Hc * d, st, &vy);
     tm.done();
     if (s != TSF_OK) return s;
   }
-  const __half* sxt = h->xt;
-  if (P > 1) {
-    StageTimer tm(h, st, 2);
-    s = all_to_all_xt(h, st);
-    tm.done();
-    if (s != TSF_OK) return s;
-    sxt = h->uxt;
-  }
-  // spatial stage: y = X_t + S(X_t, X_t, X_t)
-  StageTimer tm(h, st, 1);
-  s = run_attention(h, spatial_view(Kl, h->N, h->H, h->d), sxt, sxt, sxt, EPI_BLOCK_S, nullptr, y, st);
-  tm.done();
-  return s;
+  return TSF_OK;
 }
 
 tsf_status tsf_spacetime_block_host(tsf_handle* h, const tsf_bf16* x_host, float* y_host, void* stream) {
