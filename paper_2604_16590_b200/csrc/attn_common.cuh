@@ -66,6 +66,17 @@ struct AttnParams {
   int n_qpairs, nkv;
   // diagnostics (builds with -DTSF_TRACE only): clock64 stamps of CTA 0
   unsigned long long* trace;
+  // distributed block, temporal stage (P > 1): X_t rows of frame l go straight
+  // to rank l / Kc's frame-shard buffer (NVLink, CUDA IPC mapping):
+  // peer_out[r] + (l % Kc) * osL + a * osA + (b + b_off) * osB
+  int P, Kc, b_off;
+  void* peer_out[8];
+};
+
+constexpr int MAX_PEERS = 8;
+// per-destination output tensor maps (packed kernel, distributed temporal stage)
+struct PeerMaps {
+  CUtensorMap m[MAX_PEERS];
 };
 
 #ifdef TSF_TRACE
@@ -189,6 +200,30 @@ __device__ __forceinline__ void epilogue_row_smem(const float* o_acc, float inv_
       w.w = pack2<true>(x3.x + v[6], x3.y + v[7]);
     }
     *ptr = w;
+  }
+}
+
+// EPI_BLOCK_T epilogue into a separate staging tile: x from res_tile row r,
+// X_t = fp16(x + O/l) written to row orow of out_tile (same swizzled layout).
+template <int D, int ROWS_IN, int ROWS_OUT>
+__device__ __forceinline__ void epilogue_row_stage(const float* o_acc, float inv_l, const uint8_t* res_tile,
+                                                   uint32_t r, uint8_t* out_tile, uint32_t orow) {
+  constexpr int SWB = (2 * D < 128) ? 2 * D : 128;
+  constexpr int UPC = SWB / 16;
+#pragma unroll
+  for (int u = 0; u < D / 8; ++u) {
+    const uint4 rr = tile_row_u4<D, ROWS_IN>(res_tile, r, u);
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = o_acc[8 * u + i] * inv_l;
+    const float2 x0 = unpack2<true>(rr.x), x1 = unpack2<true>(rr.y), x2 = unpack2<true>(rr.z),
+                 x3 = unpack2<true>(rr.w);
+    uint4 w;
+    w.x = pack2<true>(x0.x + v[0], x0.y + v[1]);
+    w.y = pack2<true>(x1.x + v[2], x1.y + v[3]);
+    w.z = pack2<true>(x2.x + v[4], x2.y + v[5]);
+    w.w = pack2<true>(x3.x + v[6], x3.y + v[7]);
+    *reinterpret_cast<uint4*>(out_tile + (u / UPC) * (ROWS_OUT * SWB) + swz_off<SWB>(orow, u % UPC)) = w;
   }
 }
 

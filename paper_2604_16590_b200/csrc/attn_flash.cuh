@@ -361,8 +361,18 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     }
     const int l_idx = qp * 256 + t * 128 + (int)row;
     if (l_idx < L) {
-      const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
-      epilogue_row<D, 128, EPI>(p, o, 1.0f / l_run, off, sQ + t * C::TILE_BYTES, row);
+      if (EPI == EPI_BLOCK_T && p.P > 1) {
+        // distributed temporal stage: frame l_idx belongs to rank l_idx / Kc
+        const int dst = l_idx / p.Kc;
+        AttnParams q = p;
+        q.o = p.peer_out[dst];
+        const long long off = (long long)(l_idx - dst * p.Kc) * p.osL + (long long)ga * p.osA +
+                              (long long)(gb + p.b_off) * p.osB;
+        epilogue_row<D, 128, EPI>(q, o, 1.0f / l_run, off, sQ + t * C::TILE_BYTES, row);
+      } else {
+        const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
+        epilogue_row<D, 128, EPI>(p, o, 1.0f / l_run, off, sQ + t * C::TILE_BYTES, row);
+      }
     }
   } else {
     // ===================== converter warp 11 (block temporal stage) =====================

@@ -30,6 +30,8 @@ struct PackedCfg {
   static constexpr int TCOLS = (192 + D <= 256) ? 256 : 512;  // S(128) + P(64) + O(D)
   static constexpr int COL_S = 0, COL_P = 128, COL_O = 192;
   static constexpr int SMEM = NST * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  // + one output staging tile when the distributed temporal stage scatters X_t
+  static constexpr int SMEM_DIST = SMEM + TILE_BYTES;
   static constexpr int THREADS = 192;
 };
 
@@ -37,7 +39,7 @@ template <int D, int WIN, int EPI, bool SHARED, int NST>
 __global__ void __launch_bounds__(192, (192 + D <= 256) ? 2 : 1)
 attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                    const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap to,
-                   const AttnParams p) {
+                   const __grid_constant__ PeerMaps pm, const AttnParams p) {
   using C = PackedCfg<D, WIN, EPI, SHARED, NST>;
   constexpr bool F16 = EpiTraits<EPI>::F16;
   constexpr bool CONVERT = EpiTraits<EPI>::CONVERT;
@@ -49,6 +51,7 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * C::STAGE_BYTES);
+  uint8_t* stage_out = smem + NST * C::STAGE_BYTES + 1024;  // distributed temporal stage only (1024-aligned)
   uint64_t* full = bars;               // [NST] TMA -> MMA
   uint64_t* empty = bars + NST;        // [NST] epilogue -> TMA
   uint64_t* s_full = bars + 2 * NST;   // MMA -> softmax
@@ -250,7 +253,29 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
       if (lane == 0) mbar_arrive(o_empty);
 
       const int a0 = (tile % p.tiles_a) * p.Ab, b0 = (tile / p.tiles_a) * p.Bb;
-      if constexpr (TMA_OUT) {
+      if (EPI == EPI_BLOCK_T && p.P > 1) {
+        // distributed: rows regrouped by destination rank (frame l -> rank
+        // l / Kc) into P dense boxes of Kc * G rows, one TMA store per rank
+        // straight into that rank's frame shard (NVLink peer memory)
+        const int Kc = p.Kc, rows_per_dst = Kc * G;
+        if (threadIdx.x == 0) bulk_wait_read0();   // previous tile's stores have read the staging tile
+        named_bar_sync(1, 128);
+        if (row_ok) {
+          const int dst = li / Kc, orow = dst * rows_per_dst + (li - dst * Kc) + Kc * gi;
+          epilogue_row_stage<D, 128, 128>(o, 1.0f / l, smem + s * C::STAGE_BYTES, r, stage_out, orow);
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (threadIdx.x == 0) {
+          mbar_arrive(&empty[s]);                  // the input stage is no longer read
+          for (int dst = 0; dst < p.P; ++dst)
+#pragma unroll
+            for (int c = 0; c < C::NCH; ++c)
+              tma_store_4d(&pm.m[dst], stage_out + c * C::CHUNK_BYTES + dst * rows_per_dst * C::SWB, c * C::CH, 0,
+                           a0, b0);
+          bulk_commit();
+        }
+      } else if constexpr (TMA_OUT) {
         // rows into the stage's (first) tile in place, then one TMA store
         if (row_ok) epilogue_row_smem<D, 128, EPI>(o, 1.0f / l, smem + s * C::STAGE_BYTES, r);
         fence_proxy_async_smem();

@@ -48,6 +48,18 @@ struct tsf_handle {
   int nchunk = 1;
   cudaStream_t comm_stream = nullptr;
   std::vector<cudaEvent_t> ev_t, ev_a;
+  // fused exchange: every rank's frame-shard X_t buffer (uxt) mapped here
+  // through CUDA IPC; the temporal kernel stores X_t rows straight into them
+  void* peer_uxt[MAX_PEERS] = {};
+  bool fused = false;
+  int* d_flag = nullptr;        // 1-int NCCL all-reduce = cross-rank barrier
+  PeerMaps pm{};                // per-destination output maps of the current launch
+  bool use_pm = false;
+};
+
+// Output routing of the distributed temporal stage (run_attention).
+struct DistOut {
+  int P, Kc, rank, Nl;
 };
 
 static thread_local std::string g_create_err;
@@ -180,10 +192,12 @@ static tsf_status launch_packed_t(tsf_handle* h, cudaStream_t st, const CUtensor
                                   const CUtensorMap& mv, const CUtensorMap& mo, const AttnParams& p) {
   constexpr int NST = SHARED ? 4 : 2;
   using C = PackedCfg<D, WIN, EPI, SHARED, NST>;
-  const int per_sm = (C::TCOLS == 256 && 2 * C::SMEM <= 227 * 1024) ? 2 : 1;
+  const int smem = h->use_pm ? C::SMEM_DIST : C::SMEM;
+  const int per_sm = (C::TCOLS == 256 && 2 * smem <= 227 * 1024) ? 2 : 1;
   int grid = h->num_sms * per_sm;
   if (grid > p.num_tiles) grid = p.num_tiles;
-  return launch(h, attn_packed_kernel<D, WIN, EPI, SHARED, NST>, grid, C::THREADS, C::SMEM, st, p, mq, mk, mv, mo);
+  return launch(h, attn_packed_kernel<D, WIN, EPI, SHARED, NST>, grid, C::THREADS, smem, st, p, mq, mk, mv, mo,
+                h->pm);
 }
 
 template <int D, int EPI, int EMU>
@@ -259,14 +273,26 @@ static tsf_status dispatch_d(tsf_handle* h, bool packed, int win, int epi, cudaS
 // Attention over one view: q/k/v (q == k == v for the block stages).  The
 // output (o or y) uses the strides of `ov` (default: the input view's).
 static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, const void* k, const void* vv, int epi,
-                                void* o, float* y, cudaStream_t st, const View* ov = nullptr) {
+                                void* o, float* y, cudaStream_t st, const View* ov = nullptr,
+                                const DistOut* dist = nullptr) {
   if (!ov) ov = &v;
+  h->use_pm = false;
   const int d = h->d;
   if ((long long)v.A * v.B == 0 || v.L == 0) return TSF_OK;
   AttnParams p{};
   p.L = v.L; p.A = v.A; p.B = v.B;
   p.sL = v.sL; p.sA = v.sA; p.sB = v.sB;
   p.osL = ov->sL; p.osA = ov->sA; p.osB = ov->sB;
+  p.P = 1;
+  if (dist) {  // EPI_BLOCK_T rows of frame l go to rank l / Kc, frame shard [Kc][N][H][d]
+    p.P = dist->P;
+    p.Kc = dist->Kc;
+    p.b_off = dist->rank * dist->Nl;
+    for (int r = 0; r < dist->P; ++r) p.peer_out[r] = h->peer_uxt[r];
+    p.osL = (long long)h->N * h->H * h->d;
+    p.osA = h->d;
+    p.osB = (long long)h->H * h->d;
+  }
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
   p.o = o;
   p.y = y;
@@ -300,7 +326,20 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
     if ((s = make_map(h, &mk, k, d, v, v.L, Ab, Bb, f16)) != TSF_OK) return s;
     if ((s = make_map(h, &mv, vv, d, v, v.L, Ab, Bb, f16)) != TSF_OK) return s;
     // output map (16-bit outputs): bf16 for the standalone calls, fp16 X_t for the block
-    if (epi != EPI_BLOCK_S && (s = make_map(h, &mo, o, d, *ov, v.L, Ab, Bb, epi == EPI_BLOCK_T)) != TSF_OK) return s;
+    if (!dist && epi != EPI_BLOCK_S && (s = make_map(h, &mo, o, d, *ov, v.L, Ab, Bb, epi == EPI_BLOCK_T)) != TSF_OK)
+      return s;
+    if (dist) {
+      // one map per destination rank over its frame shard, restricted to this
+      // rank's token range: dims (d, Kc, H, N/P), base + rank * (N/P) * H * d
+      if ((dist->Kc * Ab * Bb) % 8 != 0 || v.L * Ab * Bb > 128)
+        return fail(h, TSF_ERR_UNSUPPORTED, "fused exchange needs (K/P) * groups-per-tile % 8 == 0");
+      for (int r = 0; r < dist->P; ++r) {
+        const View pv{dist->Kc, v.A, dist->Nl, p.osL, p.osA, p.osB};
+        const void* base = static_cast<const __half*>(h->peer_uxt[r]) + (size_t)dist->rank * dist->Nl * h->H * d;
+        if ((s = make_map(h, &h->pm.m[r], base, d, pv, dist->Kc, Ab, Bb, true)) != TSF_OK) return s;
+      }
+      h->use_pm = true;
+    }
   } else {
     p.n_qpairs = (v.L + 255) / 256;
     p.nkv = (v.L + 127) / 128;
@@ -453,6 +492,39 @@ tsf_status tsf_create_dist(int K, int N, int H, int d, const void* id128, int ra
       cudaEventCreateWithFlags(&h->ev_t[c], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&h->ev_a[c], cudaEventDisableTiming);
     }
+    // fused exchange: all-gather the IPC handles of every rank's uxt and map them
+    const char* fe = getenv("TSF_FUSED_EXCHANGE");
+    if (world <= MAX_PEERS && !(fe && atoi(fe) == 0)) {
+      cudaIpcMemHandle_t mine;
+      char* dh = nullptr;
+      bool ok = cudaIpcGetMemHandle(&mine, h->uxt) == cudaSuccess &&
+                cudaMalloc(&dh, (size_t)world * sizeof mine) == cudaSuccess &&
+                cudaMalloc(&h->d_flag, sizeof(int)) == cudaSuccess &&
+                cudaMemcpy(dh + rank * sizeof mine, &mine, sizeof mine, cudaMemcpyHostToDevice) == cudaSuccess;
+      std::vector<cudaIpcMemHandle_t> all(world);
+      if (ok) ok = ncclAllGather(dh + rank * sizeof mine, dh, sizeof mine, ncclUint8, h->comm, h->comm_stream) ==
+                   ncclSuccess &&
+                   cudaStreamSynchronize(h->comm_stream) == cudaSuccess &&
+                   cudaMemcpy(all.data(), dh, (size_t)world * sizeof mine, cudaMemcpyDeviceToHost) == cudaSuccess;
+      for (int p = 0; ok && p < world; ++p) {
+        if (p == rank) h->peer_uxt[p] = h->uxt;
+        else ok = cudaIpcOpenMemHandle(&h->peer_uxt[p], all[p], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+      }
+      if (dh) cudaFree(dh);
+      cudaGetLastError();
+      // every rank must agree on the mode: all-reduce (min) of the local outcome
+      int* d_ok = nullptr;
+      int v = ok ? 1 : 0;
+      if (cudaMalloc(&d_ok, sizeof(int)) == cudaSuccess &&
+          cudaMemcpy(d_ok, &v, sizeof v, cudaMemcpyHostToDevice) == cudaSuccess &&
+          ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, h->comm, h->comm_stream) == ncclSuccess &&
+          cudaStreamSynchronize(h->comm_stream) == cudaSuccess)
+        cudaMemcpy(&v, d_ok, sizeof v, cudaMemcpyDeviceToHost);
+      else
+        v = 0;
+      if (d_ok) cudaFree(d_ok);
+      h->fused = v == 1;
+    }
   }
   *out = h;
   return TSF_OK;
@@ -467,6 +539,9 @@ void tsf_destroy(tsf_handle* h) {
     else ncclCommDestroy(h->comm);
   }
   for (auto& r : h->recs) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); }
+  for (int p = 0; p < h->world && p < MAX_PEERS; ++p)
+    if (h->peer_uxt[p] && h->peer_uxt[p] != h->uxt) cudaIpcCloseMemHandle(h->peer_uxt[p]);
+  if (h->d_flag) cudaFree(h->d_flag);
   for (auto e : h->ev_t) cudaEventDestroy(e);
   for (auto e : h->ev_a) cudaEventDestroy(e);
   if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
@@ -590,6 +665,29 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
     s = run_attention(h, spatial_view(Kl, h->N, h->H, h->d), h->xt, h->xt, h->xt, EPI_BLOCK_S, nullptr, y, st);
     tm.done();
     return s;
+  }
+  if (h->fused) {
+    // Fused exchange: the temporal kernel writes X_t rows straight into the
+    // owning rank's frame shard (CUDA IPC + NVLink TMA/plain stores), a 1-int
+    // NCCL all-reduce orders every rank's stores before any spatial read.
+    const DistOut dist{P, Kl, h->rank, Nl};
+    {
+      StageTimer tm(h, st, 0);
+      s = run_attention(h, temporal_view(h->K, Nl, h->H, h->d), x, x, x, EPI_BLOCK_T, nullptr, nullptr, st,
+                        nullptr, &dist);
+      tm.done();
+    }
+    if (s == TSF_OK) {
+      StageTimer tm(h, st, 2);
+      TSF_NCCL(h, ncclAllReduce(h->d_flag, h->d_flag, 1, ncclInt32, ncclSum, h->comm, st));
+      tm.done();
+      StageTimer tm1(h, st, 1);
+      s = run_attention(h, spatial_view(Kl, h->N, h->H, h->d), h->uxt, h->uxt, h->uxt, EPI_BLOCK_S, nullptr, y, st);
+      tm1.done();
+      return s;
+    }
+    if (s != TSF_ERR_UNSUPPORTED) return s;
+    // shapes the fused scatter cannot tile: fall through to the NCCL path
   }
   // Distributed: head-chunk pipeline.  temporal(c) for all chunks on `st`;
   // exchange(c) on the comm stream after temporal(c); unpack(c) + spatial(c)
