@@ -474,8 +474,10 @@ tsf_status tsf_create_dist(int K, int N, int H, int d, const void* id128, int ra
       delete h;
       return fail(nullptr, TSF_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     }
-    // head chunks for the exchange / spatial overlap: TSF_NCHUNK or 2
-    int nc = 2;
+    // head chunks of the NCCL fallback path (exchange / spatial overlap):
+    // TSF_NCHUNK, default 1 (chunking measured slower at P = 2: NCCL's kernels
+    // and the spatial kernel compete for SMs)
+    int nc = 1;
     if (const char* e = getenv("TSF_NCHUNK")) nc = atoi(e);
     if (nc < 1) nc = 1;
     while (nc > 1 && H % nc) --nc;
