@@ -133,12 +133,14 @@ __device__ __forceinline__ uint4 tile_row_u4(const uint8_t* tile, uint32_t r, ui
 // Epilogue for one row: o_acc[0..D) = unnormalised O row, inv_l = 1/l.
 // res_tile: the row's 16-bit input (x for BLOCK_T, X_t for BLOCK_S) in shared
 // memory (the swizzled Q tile).
-template <int D, int ROWS, int EPI>
+// NU 16-byte units starting at unit u0 (o_acc holds those 8 * NU values).
+template <int D, int ROWS, int EPI, int NU = D / 8>
 __device__ __forceinline__ void epilogue_row(const AttnParams& p, const float* o_acc, float inv_l,
-                                             long long off, const uint8_t* res_tile, uint32_t r) {
+                                             long long off, const uint8_t* res_tile, uint32_t r, int u0 = 0) {
   constexpr bool F16 = EpiTraits<EPI>::F16;
+  off += 8 * u0;
 #pragma unroll
-  for (int u = 0; u < D / 8; ++u) {
+  for (int u = 0; u < NU; ++u) {
     float v[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[i] = o_acc[8 * u + i] * inv_l;
@@ -150,7 +152,7 @@ __device__ __forceinline__ void epilogue_row(const AttnParams& p, const float* o
       w.w = pack2<false>(v[6], v[7]);
       *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o) + off + 8 * u) = w;
     } else {
-      const uint4 rr = tile_row_u4<D, ROWS>(res_tile, r, u);
+      const uint4 rr = tile_row_u4<D, ROWS>(res_tile, r, u0 + u);
       const float2 x0 = unpack2<F16>(rr.x), x1 = unpack2<F16>(rr.y), x2 = unpack2<F16>(rr.z),
                    x3 = unpack2<F16>(rr.w);
       if constexpr (EPI == EPI_BLOCK_S) {

@@ -49,7 +49,10 @@ constexpr float RESCALE_LOG2 = 8.0f;
 // barriers): measured slower at C2 (0.78 vs 0.75 ms), kept switchable.
 constexpr bool PINGPONG = false;
 
-template <int D, int EPI, int NST>
+// SPLIT = warps per tile row: 1, or 2 (d = 64: each warp of a pair takes 32 of
+// a sub-step's 64 columns, row maxima exchanged through shared memory) to put
+// four softmax warps on every SM sub-partition.
+template <int D, int EPI, int NST, int SPLIT = 1>
 struct FlashCfg {
   static constexpr int SWB = (2 * D < 128) ? 2 * D : 128;
   static constexpr int CH = SWB / 2;
@@ -61,8 +64,13 @@ struct FlashCfg {
   static constexpr int STAGE_BYTES = (SHARED ? 1 : 2) * TILE_BYTES;  // K (+ V)
   static constexpr bool ONES = (D <= 64);               // l via an MMA against a ones column
   static constexpr int ONES_BYTES = 1024;
-  static constexpr int SMEM = Q_BYTES + NST * STAGE_BYTES + ONES_BYTES + 1024 + 256;
-  static constexpr int THREADS = 384;  // 3 warpgroups (setmaxnreg is per warpgroup)
+  static constexpr int XMAX_BYTES = (SPLIT > 1) ? 2 * 2 * 2 * 128 * 4 : 0;  // [tile][half][parity][row]
+  static constexpr int SMEM = Q_BYTES + NST * STAGE_BYTES + ONES_BYTES + XMAX_BYTES + 1024 + 256;
+  static constexpr int NSW = 8 * SPLIT;                    // softmax warps
+  static constexpr int W_TMA = NSW, W_MMA0 = NSW + 1, W_MMA1 = NSW + 2, W_CONV = NSW + 3;
+  static constexpr int THREADS = 32 * (NSW + 4);          // whole warpgroups (setmaxnreg is per warpgroup)
+  static constexpr int REG_SOFTMAX = (SPLIT == 1) ? 224 : 112, REG_PRODUCER = 56;
+  static_assert(SPLIT == 1 || (D == 64 && ONES), "column split: d = 64 (l from the ones-column MMA)");
   static constexpr uint32_t OW = ONES ? D + 16 : D;
   // S buffers: tile t, buffer b at column 128 t + 64 b (64 fp32 columns); P
   // (64 16-bit values = 32 columns) overwrites the buffer's upper half.
@@ -70,11 +78,11 @@ struct FlashCfg {
   static_assert(COL_O1 + OW <= 512, "TMEM budget");
 };
 
-template <int D, int EPI, int NST, int EMU>
-__global__ void __launch_bounds__(384, 1)
+template <int D, int EPI, int NST, int EMU, int SPLIT>
+__global__ void __launch_bounds__(32 * (8 * SPLIT + 4), 1)
 attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                   const __grid_constant__ CUtensorMap tv, const AttnParams p) {
-  using C = FlashCfg<D, EPI, NST>;
+  using C = FlashCfg<D, EPI, NST, SPLIT>;
   constexpr bool F16 = EpiTraits<EPI>::F16;
   constexpr bool CONVERT = EpiTraits<EPI>::CONVERT;
   constexpr bool SHARED = C::SHARED;
@@ -83,7 +91,8 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
   uint8_t* sQ = smem;                        // Q0 | Q1
   uint8_t* sKV = smem + C::Q_BYTES;          // NST x (K | V)
   uint8_t* sOnes = sKV + NST * C::STAGE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES);
+  float* xmax = reinterpret_cast<float*>(sOnes + C::ONES_BYTES);  // SPLIT > 1: partial row maxima
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES + C::XMAX_BYTES);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;               // [NST]
   uint64_t* v_full = k_full + NST;           // [NST]
@@ -120,7 +129,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     mbar_init(q_conv, 1);
     for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&p_full[i], 4 * SPLIT);
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&o_full[t], 1);
@@ -128,7 +137,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     }
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<512>(tmem_holder);
+  if (warp == C::W_MMA0) tmem_alloc<512>(tmem_holder);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -136,9 +145,9 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
 
   // registers (setmaxnreg, per role branch): softmax warpgroups 224/thread,
   // producer warpgroup (TMA, MMA, 2 converter warps) 56/thread
-  if (warp == 8) {
+  if (warp == C::W_TMA) {
     // ===================== TMA producer =====================
-    reg_dealloc<56>();
+    reg_dealloc<C::REG_PRODUCER>();
     if (elect_one()) {
       tma_prefetch_desc(&tq);
       tma_prefetch_desc(&tk);
@@ -167,10 +176,10 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       }
     }
     __syncwarp();
-  } else if (warp == 9 || warp == 10) {
-    // ===================== MMA issuers: warp 9 -> tile 0, warp 10 -> tile 1 =====================
-    reg_dealloc<56>();
-    const int t = warp - 9;
+  } else if (warp == C::W_MMA0 || warp == C::W_MMA1) {
+    // ===================== MMA issuers: one per query tile =====================
+    reg_dealloc<C::REG_PRODUCER>();
+    const int t = warp - C::W_MMA0;
     if (elect_one()) {
       constexpr uint32_t idesc_qk = make_idesc(128, 64, 0, 0, F16);
       constexpr uint32_t idesc_pv = make_idesc(128, D, 0, 1, F16);
@@ -238,10 +247,13 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       }
     }
     __syncwarp();
-  } else if (warp < 8) {
-    // ===================== softmax warpgroups (warps 0-7) =====================
-    reg_alloc<224>();
-    const int t = warp >> 2;                                   // query tile of this warpgroup
+  } else if (warp < C::NSW) {
+    // ===================== softmax warps =====================
+    reg_alloc<C::REG_SOFTMAX>();
+    constexpr int CW = 64 / SPLIT;                             // sub-step columns per warp
+    const int t = warp / (4 * SPLIT);                          // query tile
+    const int hf = (warp >> 2) % SPLIT;                        // column half (SPLIT = 2)
+    const int c_off = CW * hf;
     const uint32_t row = (warp & 3) * 32 + lane;               // tile row == TMEM lane
     const uint32_t lane_base = ((warp & 3) * 32) << 16;
     const uint32_t tSrow = tmem + lane_base + 128 * t;
@@ -256,24 +268,30 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       mbar_wait(&s_full[2 * t + (i & 1)], (i >> 1) & 1);
       TSF_STAMP(p, warp, 6 * i + 1);
       tc_fence_after();
-      uint32_t sv[64];
-      tmem_ld_x32(tSb, sv);
-      tmem_ld_x32(tSb + 32, sv + 32);
+      uint32_t sv[CW];
+#pragma unroll
+      for (int c = 0; c < CW; c += 32) tmem_ld_x32(tSb + c_off + c, sv + c);
       tmem_wait_ld();
       TSF_STAMP(p, warp, 6 * i + 2);
-      const int valid = L - i * 64;  // columns >= valid are beyond the sequence
-      if (valid < 64) {
+      const int valid = L - i * 64 - c_off;  // columns >= valid are beyond the sequence
+      if (valid < CW) {
 #pragma unroll
-        for (int c = 0; c < 64; ++c) sv[c] = (c < valid) ? sv[c] : 0xFF800000u;  // -inf
+        for (int c = 0; c < CW; ++c) sv[c] = (c < valid) ? sv[c] : 0xFF800000u;  // -inf
       }
       // row max: 4 independent FMNMX3 chains
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < 64; c += 8)
+      for (int c = 0; c < CW; c += 8)
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           m4[q] = max3(m4[q], __uint_as_float(sv[c + 2 * q]), __uint_as_float(sv[c + 2 * q + 1]));
-      const float mx = max3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
+      float mx = max3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
+      if constexpr (SPLIT > 1) {
+        // combine with the partner warp's half of the row (parity-buffered slots)
+        xmax[((t * 2 + hf) * 2 + (i & 1)) * 128 + row] = mx;
+        named_bar_sync(3 + t * 4 + (warp & 3), 64);
+        mx = fmaxf(mx, xmax[((t * 2 + (1 - hf)) * 2 + (i & 1)) * 128 + row]);
+      }
       const float m_new = fmaxf(m_run, mx * sl2);
       TSF_STAMP(p, warp, 6 * i + 3);
       if (i == 0) {
@@ -289,15 +307,15 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           mbar_wait(&o_full[t], (i - 1) & 1);
           tc_fence_after();
 #pragma unroll
-          for (int c = 0; c < D; c += 32) {
+          for (int c = 0; c < D / SPLIT; c += 32) {   // this warp's share of O's columns
             uint32_t ov[32];
-            tmem_ld_x32(tOrow + c, ov);
+            tmem_ld_x32(tOrow + hf * (D / SPLIT) + c, ov);
             tmem_wait_ld();
 #pragma unroll
             for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            tmem_st_x32(tOrow + c, ov);
+            tmem_st_x32(tOrow + hf * (D / SPLIT) + c, ov);
           }
-          if constexpr (C::ONES) {
+          if (C::ONES && hf == 0) {
             uint32_t lv[8];
             tmem_ld_x8(tOrow + D, lv);
             tmem_wait_ld();
@@ -313,7 +331,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       const float nmb = -m_run;
       float lsum = 0.f;
 #pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 32) {
+      for (int c0 = 0; c0 < CW; c0 += 32) {
         uint32_t pk[16];
 #pragma unroll
         for (int c = c0; c < c0 + 32; c += 2) {
@@ -332,7 +350,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
             lsum += pr.x + pr.y;
           }
         }
-        tmem_st_x16(tSb + 32 + c0 / 2, pk);
+        tmem_st_x16(tSb + 32 + (c_off + c0) / 2, pk);
       }
       if (PINGPONG) named_bar_arrive(2 - t, 256);
       l_run += lsum;
@@ -348,9 +366,10 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     // ---- epilogue ----
     mbar_wait(&o_done[t], 0);
     tc_fence_after();
-    float o[D];
+    constexpr int DW = D / SPLIT;  // output columns of this warp
+    float o[DW];
 #pragma unroll
-    for (int c = 0; c < D; c += 32) tmem_ld_x32(tOrow + c, reinterpret_cast<uint32_t*>(o + c));
+    for (int c = 0; c < DW; c += 32) tmem_ld_x32(tOrow + hf * DW + c, reinterpret_cast<uint32_t*>(o + c));
     if constexpr (C::ONES) {
       uint32_t lv[8];
       tmem_ld_x8(tOrow + D, lv);
@@ -368,21 +387,21 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         q.o = p.peer_out[dst];
         const long long off = (long long)(l_idx - dst * p.Kc) * p.osL + (long long)ga * p.osA +
                               (long long)(gb + p.b_off) * p.osB;
-        epilogue_row<D, 128, EPI>(q, o, 1.0f / l_run, off, sQ + t * C::TILE_BYTES, row);
+        epilogue_row<D, 128, EPI, DW / 8>(q, o, 1.0f / l_run, off, sQ + t * C::TILE_BYTES, row, hf * DW / 8);
       } else {
         const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
-        epilogue_row<D, 128, EPI>(p, o, 1.0f / l_run, off, sQ + t * C::TILE_BYTES, row);
+        epilogue_row<D, 128, EPI, DW / 8>(p, o, 1.0f / l_run, off, sQ + t * C::TILE_BYTES, row, hf * DW / 8);
       }
     }
   } else {
-    // ===================== converter warp 11 (block temporal stage) =====================
-    reg_dealloc<56>();
+    // ===================== converter warp (block temporal stage) =====================
+    reg_dealloc<C::REG_PRODUCER>();
     if constexpr (CONVERT) {
       // bf16 tiles from TMA -> fp16 in place (rows are whole 16-byte units, so
       // the swizzle does not matter); 32 threads, one row-chunk unit at a time
       constexpr int UPR = 2 * D / 16;  // 16-byte units per row
       constexpr int UPC = C::SWB / 16;
-      const uint32_t ct = threadIdx.x - 352;
+      const uint32_t ct = threadIdx.x - 32 * C::W_CONV;
       auto convert_tile = [&](uint8_t* tile) {
         for (uint32_t i = ct; i < 128 * UPR; i += 32) {
           const uint32_t row = i / UPR, u = i % UPR;
@@ -406,7 +425,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == C::W_MMA0) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }

@@ -205,10 +205,21 @@ static tsf_status launch_flash_emu(tsf_handle* h, cudaStream_t st, const CUtenso
                                    const CUtensorMap& mv, const AttnParams& p) {
   constexpr bool SH = EpiTraits<EPI>::SHARED;
   constexpr int NST = SH ? ((D == 128) ? 4 : 8) : ((D == 128) ? 2 : 4);
-  using C = FlashCfg<D, EPI, NST>;
   const long long grid = (long long)p.n_qpairs * p.A * p.B;
   if (grid > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "grid too large");
-  return launch(h, attn_flash_kernel<D, EPI, NST, EMU>, (int)grid, C::THREADS, C::SMEM, st, p, mq, mk, mv);
+  static int split_env = -1;
+  if (split_env < 0) {
+    const char* e = getenv("TSF_SPLIT");
+    split_env = e ? atoi(e) : 2;
+  }
+  if constexpr (D == 64) {
+    if (split_env == 2) {
+      using C2 = FlashCfg<D, EPI, NST, 2>;
+      return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 2>, (int)grid, C2::THREADS, C2::SMEM, st, p, mq, mk, mv);
+    }
+  }
+  using C = FlashCfg<D, EPI, NST, 1>;
+  return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 1>, (int)grid, C::THREADS, C::SMEM, st, p, mq, mk, mv);
 }
 
 // exp2 emulation share (of 16) for the d = 64 flash kernel: TSF_EMU overrides
