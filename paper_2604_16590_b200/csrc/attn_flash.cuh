@@ -69,7 +69,10 @@ struct FlashCfg {
   static constexpr int NSW = 8 * SPLIT;                    // softmax warps
   static constexpr int W_TMA = NSW, W_MMA0 = NSW + 1, W_MMA1 = NSW + 2, W_CONV = NSW + 3;
   static constexpr int THREADS = 32 * (NSW + 4);          // whole warpgroups (setmaxnreg is per warpgroup)
-  static constexpr int REG_SOFTMAX = (SPLIT == 1) ? 224 : 112, REG_PRODUCER = 56;
+  // setmaxnreg must balance: registers the producer warpgroup releases
+  // (launch count - 56) x 128 >= what the softmax warpgroups gain.  Launch
+  // counts: 168 (384 threads), 96 (640 threads).
+  static constexpr int REG_SOFTMAX = (SPLIT == 1) ? 224 : 104, REG_PRODUCER = 56;
   static_assert(SPLIT == 1 || (D == 64 && ONES), "column split: d = 64 (l from the ones-column MMA)");
   static constexpr uint32_t OW = ONES ? D + 16 : D;
   // S buffers: tile t, buffer b at column 128 t + 64 b (64 fp32 columns); P

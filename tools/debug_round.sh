@@ -3,7 +3,7 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-run() { timeout 120 python tools/gpu_debug.py "$@" 2>&1 | tail -12; echo "[exit ${PIPESTATUS[0]}] $*"; }
+run() { timeout 60 python tools/gpu_debug.py "$@" 2>&1 | tail -12; echo "[exit ${PIPESTATUS[0]}] $*"; }
 run spatial 4 64 2 32
 run temporal 4 64 2 32
 run spatial 2 256 1 64
