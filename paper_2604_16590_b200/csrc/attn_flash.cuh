@@ -62,7 +62,11 @@ struct FlashCfg {
   static constexpr int Q_BYTES = 2 * TILE_BYTES;
   static constexpr bool SHARED = EpiTraits<EPI>::SHARED;  // block: K_j = V_j (one tile per stage)
   static constexpr int STAGE_BYTES = (SHARED ? 1 : 2) * TILE_BYTES;  // K (+ V)
-  static constexpr bool ONES = (D <= 64);               // l via an MMA against a ones column
+  // l via an MMA against a ones column: off.  Every tcgen05.mma (M=128, K=16)
+  // costs >= 44 cycles whatever its N (tools/ubench5.cu), so the N=16 ones MMA
+  // cost as much tensor time as the PV MMA itself; l is summed by the softmax
+  // threads instead (FADD2 on the fp32 P before rounding).
+  static constexpr bool ONES = false;
   static constexpr int ONES_BYTES = 1024;
   static constexpr int XMAX_BYTES = (SPLIT > 1) ? 2 * 2 * 2 * 128 * 4 : 0;  // [tile][half][parity][row]
   static constexpr int SMEM = Q_BYTES + NST * STAGE_BYTES + ONES_BYTES + XMAX_BYTES + 1024 + 256;
@@ -73,7 +77,7 @@ struct FlashCfg {
   // (launch count - 56) x 128 >= what the softmax warpgroups gain.  Launch
   // counts: 168 (384 threads), 96 (640 threads).
   static constexpr int REG_SOFTMAX = (SPLIT == 1) ? 224 : 104, REG_PRODUCER = 56;
-  static_assert(SPLIT == 1 || (D == 64 && ONES), "column split: d = 64 (l from the ones-column MMA)");
+  static_assert(SPLIT == 1 || D == 64, "column split: d = 64");
   static constexpr uint32_t OW = ONES ? D + 16 : D;
   // S buffers: tile t, buffer b at column 128 t + 64 b (64 fp32 columns); P
   // (64 16-bit values = 32 columns) overwrites the buffer's upper half.
@@ -332,7 +336,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       // (MUFU-bound), so one's exps overlap the other's waits / max / stores
       if (PINGPONG && !(t == 0 && i == 0)) named_bar_sync(1 + t, 256);
       const float nmb = -m_run;
-      float lsum = 0.f;
+      float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
       for (int c0 = 0; c0 < CW; c0 += 32) {
         uint32_t pk[16];
@@ -348,14 +352,20 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
             p1 = ex2(x1);
             pk[(c - c0) / 2] = pack2<F16>(p0, p1);
           }
-          if constexpr (!C::ONES) {
-            const float2 pr = unpack2<F16>(pk[(c - c0) / 2]);
-            lsum += pr.x + pr.y;
-          }
+          if constexpr (!C::ONES) { ls0 += p0; ls1 += p1; }
         }
         tmem_st_x16(tSb + 32 + (c_off + c0) / 2, pk);
       }
       if (PINGPONG) named_bar_arrive(2 - t, 256);
+      float lsum = ls0 + ls1;
+      if constexpr (SPLIT > 1) {
+        // the row's other half: partial sums through the same parity slots
+        // (after the max exchange above the partner has consumed them)
+        named_bar_sync(3 + t * 4 + (warp & 3), 64);
+        xmax[((t * 2 + hf) * 2 + (i & 1)) * 128 + row] = lsum;
+        named_bar_sync(3 + t * 4 + (warp & 3), 64);
+        lsum += xmax[((t * 2 + (1 - hf)) * 2 + (i & 1)) * 128 + row];
+      }
       l_run += lsum;
       TSF_STAMP(p, warp, 6 * i + 4);
       tmem_wait_st();

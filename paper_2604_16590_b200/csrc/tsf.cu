@@ -210,7 +210,7 @@ static tsf_status launch_flash_emu(tsf_handle* h, cudaStream_t st, const CUtenso
   static int split_env = -1;
   if (split_env < 0) {
     const char* e = getenv("TSF_SPLIT");
-    split_env = e ? atoi(e) : 2;
+    split_env = e ? atoi(e) : 1;
   }
   if constexpr (D == 64) {
     if (split_env == 2) {
