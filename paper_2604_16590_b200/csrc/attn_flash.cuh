@@ -52,7 +52,7 @@ constexpr bool PINGPONG = false;
 // SPLIT = warps per tile row: 1, or 2 (d = 64: each warp of a pair takes 32 of
 // a sub-step's 64 columns, row maxima exchanged through shared memory) to put
 // four softmax warps on every SM sub-partition.
-template <int D, int EPI, int NST, int SPLIT = 1>
+template <int D, int EPI, int NST, int SPLIT = 1, int SUB = 64>
 struct FlashCfg {
   static constexpr int SWB = (2 * D < 128) ? 2 * D : 128;
   static constexpr int CH = SWB / 2;
@@ -70,6 +70,12 @@ struct FlashCfg {
   static constexpr int ONES_BYTES = 1024;
   static constexpr int XMAX_BYTES = (SPLIT > 1) ? 2 * 2 * 2 * 128 * 4 : 0;  // [tile][half][parity][row]
   static constexpr int SMEM = Q_BYTES + NST * STAGE_BYTES + ONES_BYTES + XMAX_BYTES + 1024 + 256;
+  // SUB = KV columns per sub-step: 64 (S double-buffered per tile, N=64 QK^T
+  // MMAs) or 128 (one S buffer per tile, N=128 QK^T MMAs: full-rate
+  // instructions, but S(i+1) is issued only after PV(i) has consumed P(i))
+  static_assert(SUB == 64 || SUB == 128, "sub-step width");
+  static constexpr int NBUF = 128 / SUB;                  // S buffers per tile
+  static constexpr int LA = NBUF;                         // S look-ahead in sub-steps
   static constexpr int NSW = 8 * SPLIT;                    // softmax warps
   static constexpr int W_TMA = NSW, W_MMA0 = NSW + 1, W_MMA1 = NSW + 2, W_CONV = NSW + 3;
   static constexpr int THREADS = 32 * (NSW + 4);          // whole warpgroups (setmaxnreg is per warpgroup)
@@ -85,11 +91,15 @@ struct FlashCfg {
   static_assert(COL_O1 + OW <= 512, "TMEM budget");
 };
 
-template <int D, int EPI, int NST, int EMU, int SPLIT>
+template <int D, int EPI, int NST, int EMU, int SPLIT, int SUB>
 __global__ void __launch_bounds__(32 * (8 * SPLIT + 4), 1)
 attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                   const __grid_constant__ CUtensorMap tv, const AttnParams p) {
-  using C = FlashCfg<D, EPI, NST, SPLIT>;
+  using C = FlashCfg<D, EPI, NST, SPLIT, SUB>;
+  constexpr int NBUF = C::NBUF, LA = C::LA;
+  // sub-step i: S buffer b(i), barrier parity ph(i) (each buffer completes once per NBUF sub-steps)
+  auto bufi = [](int i) { return (NBUF == 2) ? (i & 1) : 0; };
+  auto phase = [](int i) { return (NBUF == 2) ? ((i >> 1) & 1) : (i & 1); };
   constexpr bool F16 = EpiTraits<EPI>::F16;
   constexpr bool CONVERT = EpiTraits<EPI>::CONVERT;
   constexpr bool SHARED = C::SHARED;
@@ -114,7 +124,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int L = p.L, nkv = p.nkv;
-  const int nsub = (L + 63) / 64;  // 64-column sub-steps (two per 128-row KV tile)
+  const int nsub = (L + SUB - 1) / SUB;  // SUB-column sub-steps (128 / SUB per 128-row KV tile)
   const int qp = blockIdx.x % p.n_qpairs;
   const int grp = blockIdx.x / p.n_qpairs;
   const int ga = grp % p.A, gb = grp / p.A;
@@ -188,7 +198,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     reg_dealloc<C::REG_PRODUCER>();
     const int t = warp - C::W_MMA0;
     if (elect_one()) {
-      constexpr uint32_t idesc_qk = make_idesc(128, 64, 0, 0, F16);
+      constexpr uint32_t idesc_qk = make_idesc(128, SUB, 0, 0, F16);
       constexpr uint32_t idesc_pv = make_idesc(128, D, 0, 1, F16);
       constexpr uint32_t idesc_l = make_idesc(128, 16, 0, 1, F16);
       constexpr uint32_t swz = (C::SWB == 128) ? SWZ_128B : SWZ_64B;
@@ -196,25 +206,27 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       const uint64_t ones_desc = make_sdesc(smem_u32(sOnes), 128, 128, SWZ_NONE);
       // S_t(i) = Q_t K_{rows 64i..64i+63}^T  -> S buffer (t, i % 2)
       auto issue_s = [&](int t, int i) {
-        const uint32_t ka = smem_u32(sKV + ((i >> 1) % NST) * C::STAGE_BYTES) + (i & 1) * 64 * C::SWB;
+        const int j = i * SUB / 128, half = (i * SUB) % 128;
+        const uint32_t ka = smem_u32(sKV + (j % NST) * C::STAGE_BYTES) + half * C::SWB;
         const uint32_t qa = q_addr + t * C::TILE_BYTES;
-        const uint32_t dS = tmem + 128 * t + 64 * (i & 1);
+        const uint32_t dS = tmem + 128 * t + SUB * bufi(i);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k * 16 / C::CH) * C::CHUNK_BYTES + (k * 16 % C::CH) * 2;
           mma_ss(dS, make_sdesc(qa + off, 16, 8 * C::SWB, swz), make_sdesc(ka + off, 16, 8 * C::SWB, swz),
                  idesc_qk, k > 0);
         }
-        mma_commit(&s_full[2 * t + (i & 1)]);
+        mma_commit(&s_full[2 * t + bufi(i)]);
       };
       // O_t += P_t(i) V_{rows 64i..64i+63} (+ l_t += P_t(i) 1)
       auto issue_pv = [&](int t, int i) {
-        const uint32_t va = smem_u32(sKV + ((i >> 1) % NST) * C::STAGE_BYTES + (SHARED ? 0 : C::TILE_BYTES)) +
-                            (i & 1) * 64 * C::SWB;
-        const uint32_t aP = tmem + 128 * t + 64 * (i & 1) + 32;
+        const int j = i * SUB / 128, half = (i * SUB) % 128;
+        const uint32_t va = smem_u32(sKV + (j % NST) * C::STAGE_BYTES + (SHARED ? 0 : C::TILE_BYTES)) +
+                            half * C::SWB;
+        const uint32_t aP = tmem + 128 * t + SUB * bufi(i) + SUB / 2;
         const uint32_t dO = tmem + (t ? C::COL_O1 : C::COL_O0);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < SUB / 16; ++k) {
           const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
           mma_ts(dO, aP + 8 * k, make_sdesc(va + k * 16 * C::SWB, C::CHUNK_BYTES, 8 * C::SWB, swz), idesc_pv, acc);
           if constexpr (C::ONES) mma_ts(dO + D, aP + 8 * k, ones_desc, idesc_l, acc);
@@ -236,20 +248,20 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       else mbar_wait(q_full, 0);
       wait_k(0);
       tc_fence_after();
-      issue_s(t, 0);
-      if (nsub > 1) issue_s(t, 1);
+      constexpr int SPT = 128 / SUB;  // sub-steps per KV tile
+      for (int i = 0; i < LA && i < nsub; ++i) issue_s(t, i);
       for (int i = 0; i < nsub; ++i) {
-        const int j = i >> 1;
-        if ((i & 1) == 0) wait_v(j);
-        const bool last_of_tile = (i & 1) || i == nsub - 1;
-        const bool more = i + 2 < nsub;
-        if (more && ((i + 2) & 1) == 0) wait_k((i + 2) >> 1);
-        mbar_wait(&p_full[2 * t + (i & 1)], (i >> 1) & 1);
+        const int j = i / SPT;
+        if (i % SPT == 0) wait_v(j);
+        const bool last_of_tile = (i % SPT == SPT - 1) || i == nsub - 1;
+        const bool more = i + LA < nsub;
+        if (more && (i + LA) % SPT == 0) wait_k((i + LA) / SPT);
+        mbar_wait(&p_full[2 * t + bufi(i)], phase(i));
         TSF_STAMP(p, warp, 2 * i);
         tc_fence_after();
         issue_pv(t, i);
         if (last_of_tile) mma_commit(&kv_empty[j % NST]);  // K_j/V_j free once both tiles' MMAs retire
-        if (more) issue_s(t, i + 2);   // reuses buffer i % 2 after PV_t(i) (same issuer: in order)
+        if (more) issue_s(t, i + LA);  // reuses buffer b(i) after PV_t(i) (same issuer: in order)
         TSF_STAMP(p, warp, 2 * i + 1);
       }
     }
@@ -257,7 +269,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
   } else if (warp < C::NSW) {
     // ===================== softmax warps =====================
     reg_alloc<C::REG_SOFTMAX>();
-    constexpr int CW = 64 / SPLIT;                             // sub-step columns per warp
+    constexpr int CW = SUB / SPLIT;                            // sub-step columns per warp
     const int t = warp / (4 * SPLIT);                          // query tile
     const int hf = (warp >> 2) % SPLIT;                        // column half (SPLIT = 2)
     const int c_off = CW * hf;
@@ -270,9 +282,9 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     float l_run = 0.f;        // used when !ONES
 
     for (int i = 0; i < nsub; ++i) {
-      const uint32_t tSb = tSrow + 64 * (i & 1);
+      const uint32_t tSb = tSrow + SUB * bufi(i);
       TSF_STAMP(p, warp, 6 * i + 0);
-      mbar_wait(&s_full[2 * t + (i & 1)], (i >> 1) & 1);
+      mbar_wait(&s_full[2 * t + bufi(i)], phase(i));
       TSF_STAMP(p, warp, 6 * i + 1);
       tc_fence_after();
       uint32_t sv[CW];
@@ -280,7 +292,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       for (int c = 0; c < CW; c += 32) tmem_ld_x32(tSb + c_off + c, sv + c);
       tmem_wait_ld();
       TSF_STAMP(p, warp, 6 * i + 2);
-      const int valid = L - i * 64 - c_off;  // columns >= valid are beyond the sequence
+      const int valid = L - i * SUB - c_off;  // columns >= valid are beyond the sequence
       if (valid < CW) {
 #pragma unroll
         for (int c = 0; c < CW; ++c) sv[c] = (c < valid) ? sv[c] : 0xFF800000u;  // -inf
@@ -311,7 +323,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           const float alpha = ex2(m_run - m_new);
           l_run *= alpha;
           m_run = m_new;
-          mbar_wait(&o_full[t], (i - 1) & 1);
+          if (NBUF == 2) mbar_wait(&o_full[t], (i - 1) & 1);  // NBUF == 1: S(i) was issued after PV(i-1)
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < D / SPLIT; c += 32) {   // this warp's share of O's columns
@@ -354,7 +366,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           }
           if constexpr (!C::ONES) { ls0 += p0; ls1 += p1; }
         }
-        tmem_st_x16(tSb + 32 + (c_off + c0) / 2, pk);
+        tmem_st_x16(tSb + SUB / 2 + (c_off + c0) / 2, pk);
       }
       if (PINGPONG) named_bar_arrive(2 - t, 256);
       float lsum = ls0 + ls1;
@@ -371,7 +383,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[2 * t + (i & 1)]);
+      if (lane == 0) mbar_arrive(&p_full[2 * t + bufi(i)]);
       TSF_STAMP(p, warp, 6 * i + 5);
     }
 

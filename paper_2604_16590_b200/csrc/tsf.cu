@@ -207,19 +207,31 @@ static tsf_status launch_flash_emu(tsf_handle* h, cudaStream_t st, const CUtenso
   constexpr int NST = SH ? ((D == 128) ? 4 : 8) : ((D == 128) ? 2 : 4);
   const long long grid = (long long)p.n_qpairs * p.A * p.B;
   if (grid > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "grid too large");
-  static int split_env = -1;
+  static int split_env = -1, sub_env = -1;
   if (split_env < 0) {
     const char* e = getenv("TSF_SPLIT");
     split_env = e ? atoi(e) : 1;
+    const char* f = getenv("TSF_SUB");
+    sub_env = f ? atoi(f) : 128;
   }
   if constexpr (D == 64) {
     if (split_env == 2) {
-      using C2 = FlashCfg<D, EPI, NST, 2>;
-      return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 2>, (int)grid, C2::THREADS, C2::SMEM, st, p, mq, mk, mv);
+      if (sub_env == 64) {
+        using C2 = FlashCfg<D, EPI, NST, 2, 64>;
+        return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 2, 64>, (int)grid, C2::THREADS, C2::SMEM, st, p, mq, mk,
+                      mv);
+      }
+      using C2 = FlashCfg<D, EPI, NST, 2, 128>;
+      return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 2, 128>, (int)grid, C2::THREADS, C2::SMEM, st, p, mq, mk,
+                    mv);
     }
   }
-  using C = FlashCfg<D, EPI, NST, 1>;
-  return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 1>, (int)grid, C::THREADS, C::SMEM, st, p, mq, mk, mv);
+  if (sub_env == 64) {
+    using C = FlashCfg<D, EPI, NST, 1, 64>;
+    return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 1, 64>, (int)grid, C::THREADS, C::SMEM, st, p, mq, mk, mv);
+  }
+  using C = FlashCfg<D, EPI, NST, 1, 128>;
+  return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 1, 128>, (int)grid, C::THREADS, C::SMEM, st, p, mq, mk, mv);
 }
 
 // exp2 emulation share (of 16) for the d = 64 flash kernel: TSF_EMU overrides
