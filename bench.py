@@ -28,6 +28,20 @@ sys.path.insert(0, ROOT)
 METRIC = "space-time tokens/s per attention layer"
 UNIT = "tokens/s"
 BASE = dict(K=8, N=4096, H=16, d=64)          # BASELINE.json configs[1] (C2)
+# --config: the default C2 is weak scaling (K = 8 per GPU); C4 is weak scaling
+# with K = 16 per GPU; C3 and C5 are strong scaling (fixed shape).
+CONFIGS = {
+    "C2": dict(K=8, N=4096, H=16, d=64, weak=True),
+    "C3": dict(K=32, N=16384, H=16, d=64, weak=False),
+    "C4": dict(K=16, N=65536, H=16, d=128, weak=True),
+    "C5": dict(K=1024, N=1024, H=8, d=64, weak=False),
+}
+
+
+def shape_for(cfg, world):
+    c = CONFIGS[cfg]
+    K = c["K"] * world if c["weak"] else c["K"]
+    return K, c["N"], c["H"], c["d"], ("weak" if c["weak"] else "strong")
 L2_BYTES = 126 * 2 ** 20
 
 
@@ -153,9 +167,14 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(K, N, H, d, world):
-    return {"workload": f"C2 per GPU (BASELINE.json configs[1]): K={K} frames (8 per GPU), N={N} tokens "
-                        f"(64x64 lat-lon patches), H={H}, d={d}, batch 1; factorized block temporal->spatial",
+def workload_config(K, N, H, d, world, cfg="C2"):
+    if cfg == "C2":
+        wl = (f"C2 per GPU (BASELINE.json configs[1]): K={K} frames (8 per GPU), N={N} tokens "
+              f"(64x64 lat-lon patches), H={H}, d={d}, batch 1; factorized block temporal->spatial")
+    else:
+        wl = (f"{cfg} (BASELINE.json configs[{'C1 C2 C3 C4 C5'.split().index(cfg)}]): K={K}, N={N}, H={H}, d={d}, "
+              f"batch 1; factorized block temporal->spatial; inputs iid N(0,1) clipped to +-4 (device-generated)")
+    return {"workload": wl,
             "K": K, "N": N, "H": H, "d": d, "global_batch": 1, "seq_len": K * N,
             "parallelism": f"axis-sharded x{world} (temporal by token, spatial by frame, 1 all-to-all)"
             if world > 1 else "single GPU",
@@ -169,6 +188,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="tsf", choices=["tsf", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -191,14 +211,18 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
-    K, N, H, d = BASE["K"] * world, BASE["N"], BASE["H"], BASE["d"]
+    K, N, H, d, scaling = shape_for(args.config, world)
     layer = tsf.Layer(K, N, H, d, group=group)
     Nl, Kl = N // world, K // world
 
     # inputs: this rank's token shard; R rotating sets so a step never finds its
     # input or output in L2 (each set 2*E + 4*E bytes per rank > L2 / R)
-    xs_bits = synth.make_x(K, N, H, d, seed=0, tokens=slice(rank * Nl, (rank + 1) * Nl))
-    x0 = synth.bits_to_torch(xs_bits, "cuda")
+    if args.config == "C2":
+        xs_bits = synth.make_x(K, N, H, d, seed=0, tokens=slice(rank * Nl, (rank + 1) * Nl))
+        x0 = synth.bits_to_torch(xs_bits, "cuda")
+    else:  # large shapes: seeded device-side iid inputs (generation is not timed)
+        g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+        x0 = torch.randn((K, Nl, H, d), generator=g, device="cuda").clamp_(-4, 4).to(torch.bfloat16)
     set_bytes = x0.numel() * 2 + Kl * N * H * d * 4
     R = max(2, int(np.ceil(3 * L2_BYTES / set_bytes)))
     xs = [x0] + [x0.clone() for _ in range(R - 1)]
@@ -276,14 +300,14 @@ def main():
         clocks = clk.summary()
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": dict(workload_config(K, N, H, d, world), l2_sets=R),
+            "config": dict(workload_config(K, N, H, d, world, args.config), l2_sets=R),
             "tflops": F / (step_ms / 1e3) / 1e12,
             "tflops_frac_of_measured": F / (step_ms / 1e3) / 1e12 / pk["tflops"],
-            "roofline": {"bound": "tensor", "kernel": "attn_flash_kernel<64, EPI_BLOCK_S> (spatial stage)",
+            "roofline": {"bound": "tensor", "kernel": f"attn_flash_kernel<{d}, EPI_BLOCK_S> (spatial stage)",
                          "achieved": achieved, "peak": pk["tflops"], "unit": "TFLOP/s",
-                         "frac": achieved / pk["tflops"], "traffic": traffic_from_profiles("spatial_C2"),
+                         "frac": achieved / pk["tflops"], "traffic": traffic_from_profiles(f"spatial_{args.config}"),
                          "peak_source": pk["source"] + " bf16 burst (fp16 operands: same nominal rate)",
                          "algorithmic_flops_per_launch": sp_flops, "launch_ms": sp_launch_ms,
                          "launches_per_step": per_step,
@@ -303,7 +327,7 @@ def main():
                            "busbw_GBs": algbw * (world - 1) / world, "nvlink_GBs_per_dir": 900,
                            "overlap": "head-chunk pipeline: exchange(c+1) overlaps spatial(c)"}
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline(8, N, H, d)
+            line["cpu_baseline"] = cpu_baseline(min(K, 8), N, H, d)
         print(json.dumps(line), flush=True)
     layer.close()
     if world > 1:
