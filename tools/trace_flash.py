@@ -39,7 +39,8 @@ def main():
     torch.cuda.synchronize()
     L.tsf_trace_read(layer._h, buf, 16 * PER_WARP)
     a = np.frombuffer(buf, dtype=np.uint64).reshape(16, PER_WARP).astype(np.int64)
-    nsub = (N + 63) // 64
+    sub = int(os.environ.get("TSF_SUB", "128"))
+    nsub = (N + sub - 1) // sub
     t0 = a[a > 0].min()
     print(f"{what} TSF_EMU={os.environ.get('TSF_EMU', 'default')} nsub={nsub}  kernel span (CTA0 stamps) {a.max() - t0} cycles")
     phases = ["wait S", "ld S", "max", "exp+st", "arrive", "to next"]
