@@ -66,10 +66,16 @@ struct FlashCfg {
   // costs >= 44 cycles whatever its N (tools/ubench5.cu), so the N=16 ones MMA
   // cost as much tensor time as the PV MMA itself; l is summed by the softmax
   // threads instead (FADD2 on the fp32 P before rounding).
-  static constexpr bool ONES = false;
-  static constexpr int ONES_BYTES = 1024;
+  // l via the PV MMA itself (d = 64): the ones column is a second MN atom of
+  // the V operand (descriptor LBO points from the V tile to a 128-row tile of
+  // ones), so one N = d + 16 MMA produces O and l = P 1 (+~8% PV time).
+  // (A separate N=16 MMA cost as much as the PV MMA: every tcgen05.mma is
+  // >= 44 cycles; summing P on the FMA pipe competes with the softmax.)
+  static constexpr bool ONES = (D == 64);
+  static constexpr int ONES_BYTES = ONES ? 128 * SWB : 0;
   static constexpr int XMAX_BYTES = (SPLIT > 1) ? 2 * 2 * 2 * 128 * 4 : 0;  // [tile][half][parity][row]
   static constexpr int SMEM = Q_BYTES + NST * STAGE_BYTES + ONES_BYTES + XMAX_BYTES + 1024 + 256;
+  static_assert(SMEM <= 227 * 1024, "shared memory");
   // SUB = KV columns per sub-step: 64 (S double-buffered per tile, N=64 QK^T
   // MMAs) or 128 (one S buffer per tile, N=128 QK^T MMAs: full-rate
   // instructions, but S(i+1) is issued only after PV(i) has consumed P(i))
@@ -199,11 +205,9 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     const int t = warp - C::W_MMA0;
     if (elect_one()) {
       constexpr uint32_t idesc_qk = make_idesc(128, SUB, 0, 0, F16);
-      constexpr uint32_t idesc_pv = make_idesc(128, D, 0, 1, F16);
-      constexpr uint32_t idesc_l = make_idesc(128, 16, 0, 1, F16);
+      constexpr uint32_t idesc_pv = make_idesc(128, C::OW, 0, 1, F16);
       constexpr uint32_t swz = (C::SWB == 128) ? SWZ_128B : SWZ_64B;
       const uint32_t q_addr = smem_u32(sQ);
-      const uint64_t ones_desc = make_sdesc(smem_u32(sOnes), 128, 128, SWZ_NONE);
       // S_t(i) = Q_t K_{rows 64i..64i+63}^T  -> S buffer (t, i % 2)
       auto issue_s = [&](int t, int i) {
         const int j = i * SUB / 128, half = (i * SUB) % 128;
@@ -224,12 +228,13 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         const uint32_t va = smem_u32(sKV + (j % NST) * C::STAGE_BYTES + (SHARED ? 0 : C::TILE_BYTES)) +
                             half * C::SWB;
         const uint32_t aP = tmem + 128 * t + SUB * bufi(i) + SUB / 2;
+        // second MN atom of the B operand: the next V chunk (d = 128) or the ones tile
+        const uint32_t vlbo = C::ONES ? smem_u32(sOnes) - va : (uint32_t)C::CHUNK_BYTES;
         const uint32_t dO = tmem + (t ? C::COL_O1 : C::COL_O0);
 #pragma unroll
         for (int k = 0; k < SUB / 16; ++k) {
           const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
-          mma_ts(dO, aP + 8 * k, make_sdesc(va + k * 16 * C::SWB, C::CHUNK_BYTES, 8 * C::SWB, swz), idesc_pv, acc);
-          if constexpr (C::ONES) mma_ts(dO + D, aP + 8 * k, ones_desc, idesc_l, acc);
+          mma_ts(dO, aP + 8 * k, make_sdesc(va + k * 16 * C::SWB, vlbo, 8 * C::SWB, swz), idesc_pv, acc);
         }
         mma_commit(&o_full[t]);
         if (i == nsub - 1) mma_commit(&o_done[t]);
@@ -370,7 +375,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       }
       if (PINGPONG) named_bar_arrive(2 - t, 256);
       float lsum = ls0 + ls1;
-      if constexpr (SPLIT > 1) {
+      if constexpr (SPLIT > 1 && !C::ONES) {
         // the row's other half: partial sums through the same parity slots
         // (after the max exchange above the partner has consumed them)
         named_bar_sync(3 + t * 4 + (warp & 3), 64);
