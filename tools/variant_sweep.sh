@@ -2,8 +2,9 @@
 # Bench flash-kernel variants: TSF_SUB (64|128) x TSF_SPLIT (1|2) x TSF_EMU.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out/var
-for v in ${VARIANTS:-"128 1 0" "128 1 4" "128 1 6" "64 1 4" "128 2 4" "128 2 6"}; do
-  set -- $v
+# VARIANTS="sub,split,emu sub,split,emu ..."
+for v in ${VARIANTS:-128,1,0 128,1,4 128,1,6 64,1,4 128,2,4 128,2,6}; do
+  set -- ${v//,/ }
   TSF_SUB=$1 TSF_SPLIT=$2 TSF_EMU=$3 timeout 120 python bench.py --steps 1000 --warmup 10 --no-cpu-baseline > gpurun_out/var/v_$1_$2_$3.json 2>&1
   python - "$1" "$2" "$3" <<'PY'
 import json, sys
