@@ -47,7 +47,7 @@ namespace tsf {
 constexpr float RESCALE_LOG2 = 8.0f;
 // Ping-pong of the two softmax warpgroups' exponential phases (named
 // barriers): measured slower at C2 (0.78 vs 0.75 ms), kept switchable.
-constexpr bool PINGPONG = false;
+constexpr bool PINGPONG = true;
 
 // SPLIT = warps per tile row: 1, or 2 (d = 64: each warp of a pair takes 32 of
 // a sub-step's 64 columns, row maxima exchanged through shared memory) to put
