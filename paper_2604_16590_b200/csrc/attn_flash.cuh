@@ -351,7 +351,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       }
       // ping-pong: the two warpgroups take turns for the exponential phase
       // (MUFU-bound), so one's exps overlap the other's waits / max / stores
-      if (PINGPONG && !(t == 0 && i == 0)) named_bar_sync(1 + t, 256);
+      if (PINGPONG && !(t == 0 && i == 0)) named_bar_sync(1 + t, 256 * SPLIT);
       const float nmb = -m_run;
       float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
@@ -373,7 +373,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         }
         tmem_st_x16(tSb + SUB / 2 + (c_off + c0) / 2, pk);
       }
-      if (PINGPONG) named_bar_arrive(2 - t, 256);
+      if (PINGPONG) named_bar_arrive(2 - t, 256 * SPLIT);
       float lsum = ls0 + ls1;
       if constexpr (SPLIT > 1 && !C::ONES) {
         // the row's other half: partial sums through the same parity slots
@@ -392,7 +392,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       TSF_STAMP(p, warp, 6 * i + 5);
     }
 
-    if (PINGPONG && t == 0) named_bar_sync(1, 256);  // consume warpgroup 1's last turn
+    if (PINGPONG && t == 0) named_bar_sync(1, 256 * SPLIT);  // consume tile 1's last turn
     // ---- epilogue ----
     mbar_wait(&o_done[t], 0);
     tc_fence_after();
