@@ -285,8 +285,16 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
           for (int c = 0; c < C::NCH; ++c)
             tma_store_4d(&to, smem + s * C::STAGE_BYTES + c * C::CHUNK_BYTES, c * C::CH, 0, a0, b0);
           bulk_commit();
-          bulk_wait_read0();          // stage may be refilled once the store has read it
-          mbar_arrive(&empty[s]);
+          // release the PREVIOUS tile's stage once its store has read smem
+          // (at most one store group in flight), so this wait overlaps work
+          if (i > 0) {
+            bulk_wait_read1();
+            mbar_arrive(&empty[(i - 1) % NST]);
+          }
+          if (i == my_tiles - 1) {
+            bulk_wait_read0();
+            mbar_arrive(&empty[s]);
+          }
         }
       } else {
         const int a = a0 + gi % p.Ab, b = b0 + gi / p.Ab;
