@@ -71,6 +71,10 @@ struct AttnParams {
   // peer_out[r] + (l % Kc) * osL + a * osA + (b + b_off) * osB
   int P, Kc, b_off;
   void* peer_out[8];
+  // flash kernel: the block residual is read from global memory (the input
+  // tensor, input-view strides): x (bf16) for EPI_BLOCK_T, X_t (fp16) for EPI_BLOCK_S
+  const void* res;
+  int num_items;  // flash kernel work items (pairs of query tiles x groups), persistent CTAs
 };
 
 constexpr int MAX_PEERS = 8;
@@ -155,6 +159,49 @@ __device__ __forceinline__ void epilogue_row(const AttnParams& p, const float* o
       const uint4 rr = tile_row_u4<D, ROWS>(res_tile, r, u0 + u);
       const float2 x0 = unpack2<F16>(rr.x), x1 = unpack2<F16>(rr.y), x2 = unpack2<F16>(rr.z),
                    x3 = unpack2<F16>(rr.w);
+      if constexpr (EPI == EPI_BLOCK_S) {
+        float4 y0, y1;
+        y0.x = x0.x + v[0]; y0.y = x0.y + v[1]; y0.z = x1.x + v[2]; y0.w = x1.y + v[3];
+        y1.x = x2.x + v[4]; y1.y = x2.y + v[5]; y1.z = x3.x + v[6]; y1.w = x3.y + v[7];
+        *reinterpret_cast<float4*>(p.y + off + 8 * u) = y0;
+        *reinterpret_cast<float4*>(p.y + off + 8 * u + 4) = y1;
+      } else {  // EPI_BLOCK_T: X_t = x + O/l, stored fp16
+        uint4 w;
+        w.x = pack2<true>(x0.x + v[0], x0.y + v[1]);
+        w.y = pack2<true>(x1.x + v[2], x1.y + v[3]);
+        w.z = pack2<true>(x2.x + v[4], x2.y + v[5]);
+        w.w = pack2<true>(x3.x + v[6], x3.y + v[7]);
+        *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.o) + off + 8 * u) = w;
+      }
+    }
+  }
+}
+
+// Flash-kernel epilogue for NU units starting at unit u0 of one row, residual
+// read from global memory at element offset in_off (EPI_BLOCK_T: bf16 x,
+// EPI_BLOCK_S: fp16 X_t); output at element offset off of p.o / p.y.
+template <int D, int EPI, int NU>
+__device__ __forceinline__ void epilogue_row_g(const AttnParams& p, const float* o_acc, float inv_l, long long off,
+                                               long long in_off, int u0) {
+  off += 8 * u0;
+  in_off += 8 * u0;
+#pragma unroll
+  for (int u = 0; u < NU; ++u) {
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = o_acc[8 * u + i] * inv_l;
+    if constexpr (EPI == EPI_OUT16) {
+      uint4 w;
+      w.x = pack2<false>(v[0], v[1]);
+      w.y = pack2<false>(v[2], v[3]);
+      w.z = pack2<false>(v[4], v[5]);
+      w.w = pack2<false>(v[6], v[7]);
+      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o) + off + 8 * u) = w;
+    } else {
+      constexpr bool RES_F16 = (EPI == EPI_BLOCK_S);
+      const uint4 rr = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(p.res) + in_off + 8 * u);
+      const float2 x0 = unpack2<RES_F16>(rr.x), x1 = unpack2<RES_F16>(rr.y), x2 = unpack2<RES_F16>(rr.z),
+                   x3 = unpack2<RES_F16>(rr.w);
       if constexpr (EPI == EPI_BLOCK_S) {
         float4 y0, y1;
         y0.x = x0.x + v[0]; y0.y = x0.y + v[1]; y0.z = x1.x + v[2]; y0.w = x1.y + v[3];

@@ -123,17 +123,27 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
   uint64_t* s_full = kv_empty + NST;         // [2 tiles][2 buffers]
   uint64_t* p_full = s_full + 4;             // [2 tiles][2 buffers]
   uint64_t* o_full = p_full + 4;             // [2] one phase per PV sub-step
-  uint64_t* o_done = o_full + 2;             // [2] last PV of the tile retired
-  uint64_t* q_conv = o_done + 2;             // converter warps -> MMA (CONVERT only)
+  uint64_t* o_done = o_full + 2;             // [2] last PV of the item retired (one phase per item)
+  uint64_t* o_empty = o_done + 2;            // [2] epilogue read O -> next item's PV may overwrite
+  uint64_t* q_empty = o_empty + 2;           // last QK^T of the item retired -> next Q may load
+  uint64_t* q_conv = q_empty + 1;            // converter warp -> MMA (CONVERT only)
   uint64_t* kv_conv = q_conv + 1;            // [NST]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(kv_conv + NST);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int L = p.L, nkv = p.nkv;
   const int nsub = (L + SUB - 1) / SUB;  // SUB-column sub-steps (128 / SUB per 128-row KV tile)
-  const int qp = blockIdx.x % p.n_qpairs;
-  const int grp = blockIdx.x / p.n_qpairs;
-  const int ga = grp % p.A, gb = grp / p.A;
+  // persistent: CTA handles work items blockIdx.x, blockIdx.x + gridDim.x, ...;
+  // item = (query-tile pair qp, group (ga, gb)), group-major so consecutive
+  // CTAs share a group's K/V in L2
+  const int my_items = (p.num_items > (int)blockIdx.x) ? (p.num_items - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  auto item_coords = [&](int k, int& qp, int& ga, int& gb) {
+    const int item = blockIdx.x + k * gridDim.x;
+    qp = item % p.n_qpairs;
+    const int grp = item / p.n_qpairs;
+    ga = grp % p.A;
+    gb = grp / p.A;
+  };
 
   if constexpr (C::ONES) {
     const uint32_t one2 = F16 ? 0x3C003C00u : 0x3F803F80u;
@@ -157,7 +167,9 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     for (int t = 0; t < 2; ++t) {
       mbar_init(&o_full[t], 1);
       mbar_init(&o_done[t], 1);
+      mbar_init(&o_empty[t], 4 * SPLIT);
     }
+    mbar_init(q_empty, 2);
     fence_barrier_init();
   }
   if (warp == C::W_MMA0) tmem_alloc<512>(tmem_holder);
@@ -175,26 +187,32 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       tma_prefetch_desc(&tq);
       tma_prefetch_desc(&tk);
       tma_prefetch_desc(&tv);
-      mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+      int g = 0;  // KV tiles loaded so far (all items)
+      for (int k = 0; k < my_items; ++k) {
+        int qp, ga, gb;
+        item_coords(k, qp, ga, gb);
+        if (k > 0) mbar_wait(q_empty, (k - 1) & 1);
+        mbar_arrive_expect_tx(q_full, C::Q_BYTES);
 #pragma unroll
-      for (int t = 0; t < 2; ++t)
-#pragma unroll
-        for (int c = 0; c < C::NCH; ++c)
-          tma_load_4d(sQ + t * C::TILE_BYTES + c * C::CHUNK_BYTES, &tq, q_full, c * C::CH,
-                      qp * 256 + t * 128, ga, gb);
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j % NST;
-        if (j >= NST) mbar_wait(&kv_empty[s], ((j / NST) - 1) & 1);
-        uint8_t* sk = sKV + s * C::STAGE_BYTES;
-        mbar_arrive_expect_tx(&k_full[s], C::TILE_BYTES);
-#pragma unroll
-        for (int c = 0; c < C::NCH; ++c)
-          tma_load_4d(sk + c * C::CHUNK_BYTES, &tk, &k_full[s], c * C::CH, j * 128, ga, gb);
-        if constexpr (!SHARED) {
-          mbar_arrive_expect_tx(&v_full[s], C::TILE_BYTES);
+        for (int t = 0; t < 2; ++t)
 #pragma unroll
           for (int c = 0; c < C::NCH; ++c)
-            tma_load_4d(sk + C::TILE_BYTES + c * C::CHUNK_BYTES, &tv, &v_full[s], c * C::CH, j * 128, ga, gb);
+            tma_load_4d(sQ + t * C::TILE_BYTES + c * C::CHUNK_BYTES, &tq, q_full, c * C::CH,
+                        qp * 256 + t * 128, ga, gb);
+        for (int j = 0; j < nkv; ++j, ++g) {
+          const int s = g % NST;
+          if (g >= NST) mbar_wait(&kv_empty[s], ((g / NST) - 1) & 1);
+          uint8_t* sk = sKV + s * C::STAGE_BYTES;
+          mbar_arrive_expect_tx(&k_full[s], C::TILE_BYTES);
+#pragma unroll
+          for (int c = 0; c < C::NCH; ++c)
+            tma_load_4d(sk + c * C::CHUNK_BYTES, &tk, &k_full[s], c * C::CH, j * 128, ga, gb);
+          if constexpr (!SHARED) {
+            mbar_arrive_expect_tx(&v_full[s], C::TILE_BYTES);
+#pragma unroll
+            for (int c = 0; c < C::NCH; ++c)
+              tma_load_4d(sk + C::TILE_BYTES + c * C::CHUNK_BYTES, &tv, &v_full[s], c * C::CH, j * 128, ga, gb);
+          }
         }
       }
     }
@@ -209,25 +227,26 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       constexpr uint32_t swz = (C::SWB == 128) ? SWZ_128B : SWZ_64B;
       const uint32_t q_addr = smem_u32(sQ);
       // S_t(i) = Q_t K_{rows 64i..64i+63}^T  -> S buffer (t, i % 2)
-      auto issue_s = [&](int t, int i) {
-        const int j = i * SUB / 128, half = (i * SUB) % 128;
+      // i: sub-step within the item, G: global sub-step (buffers/parities), g0: global index of the item's first KV tile
+      auto issue_s = [&](int t, int i, int G, int g0) {
+        const int j = g0 + i * SUB / 128, half = (i * SUB) % 128;
         const uint32_t ka = smem_u32(sKV + (j % NST) * C::STAGE_BYTES) + half * C::SWB;
         const uint32_t qa = q_addr + t * C::TILE_BYTES;
-        const uint32_t dS = tmem + 128 * t + SUB * bufi(i);
+        const uint32_t dS = tmem + 128 * t + SUB * bufi(G);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k * 16 / C::CH) * C::CHUNK_BYTES + (k * 16 % C::CH) * 2;
           mma_ss(dS, make_sdesc(qa + off, 16, 8 * C::SWB, swz), make_sdesc(ka + off, 16, 8 * C::SWB, swz),
                  idesc_qk, k > 0);
         }
-        mma_commit(&s_full[2 * t + bufi(i)]);
+        mma_commit(&s_full[2 * t + bufi(G)]);
       };
       // O_t += P_t(i) V_{rows 64i..64i+63} (+ l_t += P_t(i) 1)
-      auto issue_pv = [&](int t, int i) {
-        const int j = i * SUB / 128, half = (i * SUB) % 128;
+      auto issue_pv = [&](int t, int i, int G, int g0) {
+        const int j = g0 + i * SUB / 128, half = (i * SUB) % 128;
         const uint32_t va = smem_u32(sKV + (j % NST) * C::STAGE_BYTES + (SHARED ? 0 : C::TILE_BYTES)) +
                             half * C::SWB;
-        const uint32_t aP = tmem + 128 * t + SUB * bufi(i) + SUB / 2;
+        const uint32_t aP = tmem + 128 * t + SUB * bufi(G) + SUB / 2;
         // second MN atom of the B operand: the next V chunk (d = 128) or the ones tile
         const uint32_t vlbo = C::ONES ? smem_u32(sOnes) - va : (uint32_t)C::CHUNK_BYTES;
         const uint32_t dO = tmem + (t ? C::COL_O1 : C::COL_O0);
@@ -249,25 +268,38 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         if constexpr (!SHARED) mbar_wait(&v_full[j % NST], (j / NST) & 1);
         else wait_k(j);
       };
-      if constexpr (CONVERT) mbar_wait(q_conv, 0);
-      else mbar_wait(q_full, 0);
-      wait_k(0);
-      tc_fence_after();
       constexpr int SPT = 128 / SUB;  // sub-steps per KV tile
-      for (int i = 0; i < LA && i < nsub; ++i) issue_s(t, i);
-      for (int i = 0; i < nsub; ++i) {
-        const int j = i / SPT;
-        if (i % SPT == 0) wait_v(j);
-        const bool last_of_tile = (i % SPT == SPT - 1) || i == nsub - 1;
-        const bool more = i + LA < nsub;
-        if (more && (i + LA) % SPT == 0) wait_k((i + LA) / SPT);
-        mbar_wait(&p_full[2 * t + bufi(i)], phase(i));
-        TSF_STAMP(p, warp, 2 * i);
+      int G0 = 0, g0 = 0;             // global sub-step / KV tile index of the item's start
+      for (int k = 0; k < my_items; ++k, G0 += nsub, g0 += nkv) {
+        if constexpr (CONVERT) mbar_wait(q_conv, k & 1);
+        else mbar_wait(q_full, k & 1);
+        wait_k(g0);
         tc_fence_after();
-        issue_pv(t, i);
-        if (last_of_tile) mma_commit(&kv_empty[j % NST]);  // K_j/V_j free once both tiles' MMAs retire
-        if (more) issue_s(t, i + LA);  // reuses buffer b(i) after PV_t(i) (same issuer: in order)
-        TSF_STAMP(p, warp, 2 * i + 1);
+        for (int i = 0; i < LA && i < nsub; ++i) {
+          issue_s(t, i, G0 + i, g0);
+          if (i == nsub - 1) mma_commit(q_empty);   // Q no longer read once this retires
+        }
+        for (int i = 0; i < nsub; ++i) {
+          const int G = G0 + i, j = g0 + i / SPT;
+          if (i % SPT == 0) wait_v(j);
+          const bool last_of_tile = (i % SPT == SPT - 1) || i == nsub - 1;
+          const bool more = i + LA < nsub;
+          if (more && (i + LA) % SPT == 0) wait_k(g0 + (i + LA) / SPT);
+          mbar_wait(&p_full[2 * t + bufi(G)], phase(G));
+          TSF_STAMP(p, warp, 2 * i);
+          tc_fence_after();
+          if (i == 0 && k > 0) {  // the epilogue of the previous item has read O_t
+            mbar_wait(&o_empty[t], (k - 1) & 1);
+            tc_fence_after();
+          }
+          issue_pv(t, i, G, g0);
+          if (last_of_tile) mma_commit(&kv_empty[j % NST]);  // K_j/V_j free once both tiles' MMAs retire
+          if (more) {
+            issue_s(t, i + LA, G + LA, g0);  // reuses buffer b(G) after PV_t(G) (same issuer: in order)
+            if (i + LA == nsub - 1) mma_commit(q_empty);
+          }
+          TSF_STAMP(p, warp, 2 * i + 1);
+        }
       }
     }
     __syncwarp();
@@ -283,13 +315,18 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     const uint32_t tSrow = tmem + lane_base + 128 * t;
     const uint32_t tOrow = tmem + lane_base + (t ? C::COL_O1 : C::COL_O0);
     const float sl2 = p.scale_log2;
+    int G0 = 0;
+    for (int k = 0; k < my_items; ++k, G0 += nsub) {
+    int qp, ga, gb;
+    item_coords(k, qp, ga, gb);
     float m_run = -INFINITY;  // running max, log2-scaled units
     float l_run = 0.f;        // used when !ONES
 
     for (int i = 0; i < nsub; ++i) {
-      const uint32_t tSb = tSrow + SUB * bufi(i);
+      const int G = G0 + i;
+      const uint32_t tSb = tSrow + SUB * bufi(G);
       TSF_STAMP(p, warp, 6 * i + 0);
-      mbar_wait(&s_full[2 * t + bufi(i)], phase(i));
+      mbar_wait(&s_full[2 * t + bufi(G)], phase(G));
       TSF_STAMP(p, warp, 6 * i + 1);
       tc_fence_after();
       uint32_t sv[CW];
@@ -312,9 +349,9 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       float mx = max3(m4[0], m4[1], fmaxf(m4[2], m4[3]));
       if constexpr (SPLIT > 1) {
         // combine with the partner warp's half of the row (parity-buffered slots)
-        xmax[((t * 2 + hf) * 2 + (i & 1)) * 128 + row] = mx;
+        xmax[((t * 2 + hf) * 2 + (G & 1)) * 128 + row] = mx;
         named_bar_sync(3 + t * 4 + (warp & 3), 64);
-        mx = fmaxf(mx, xmax[((t * 2 + (1 - hf)) * 2 + (i & 1)) * 128 + row]);
+        mx = fmaxf(mx, xmax[((t * 2 + (1 - hf)) * 2 + (G & 1)) * 128 + row]);
       }
       const float m_new = fmaxf(m_run, mx * sl2);
       TSF_STAMP(p, warp, 6 * i + 3);
@@ -328,7 +365,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           const float alpha = ex2(m_run - m_new);
           l_run *= alpha;
           m_run = m_new;
-          if (NBUF == 2) mbar_wait(&o_full[t], (i - 1) & 1);  // NBUF == 1: S(i) was issued after PV(i-1)
+          if (NBUF == 2) mbar_wait(&o_full[t], (G - 1) & 1);  // NBUF == 1: S(i) was issued after PV(i-1)
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < D / SPLIT; c += 32) {   // this warp's share of O's columns
@@ -351,7 +388,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       }
       // ping-pong: the two warpgroups take turns for the exponential phase
       // (MUFU-bound), so one's exps overlap the other's waits / max / stores
-      if (PINGPONG && !(t == 0 && i == 0)) named_bar_sync(1 + t, 256 * SPLIT);
+      if (PINGPONG && !(t == 0 && G == 0)) named_bar_sync(1 + t, 256 * SPLIT);
       const float nmb = -m_run;
       float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
@@ -379,22 +416,21 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         // the row's other half: partial sums through the same parity slots
         // (after the max exchange above the partner has consumed them)
         named_bar_sync(3 + t * 4 + (warp & 3), 64);
-        xmax[((t * 2 + hf) * 2 + (i & 1)) * 128 + row] = lsum;
+        xmax[((t * 2 + hf) * 2 + (G & 1)) * 128 + row] = lsum;
         named_bar_sync(3 + t * 4 + (warp & 3), 64);
-        lsum += xmax[((t * 2 + (1 - hf)) * 2 + (i & 1)) * 128 + row];
+        lsum += xmax[((t * 2 + (1 - hf)) * 2 + (G & 1)) * 128 + row];
       }
       l_run += lsum;
       TSF_STAMP(p, warp, 6 * i + 4);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[2 * t + bufi(i)]);
+      if (lane == 0) mbar_arrive(&p_full[2 * t + bufi(G)]);
       TSF_STAMP(p, warp, 6 * i + 5);
     }
 
-    if (PINGPONG && t == 0) named_bar_sync(1, 256 * SPLIT);  // consume tile 1's last turn
-    // ---- epilogue ----
-    mbar_wait(&o_done[t], 0);
+    // ---- epilogue of item k ----
+    mbar_wait(&o_done[t], k & 1);
     tc_fence_after();
     constexpr int DW = D / SPLIT;  // output columns of this warp
     float o[DW];
@@ -408,8 +444,12 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     } else {
       tmem_wait_ld();
     }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&o_empty[t]);  // the next item's PV may overwrite O_t
     const int l_idx = qp * 256 + t * 128 + (int)row;
     if (l_idx < L) {
+      const long long in_off = (long long)l_idx * p.sL + (long long)ga * p.sA + (long long)gb * p.sB;
       if (EPI == EPI_BLOCK_T && p.P > 1) {
         // distributed temporal stage: frame l_idx belongs to rank l_idx / Kc
         const int dst = l_idx / p.Kc;
@@ -417,12 +457,14 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         q.o = p.peer_out[dst];
         const long long off = (long long)(l_idx - dst * p.Kc) * p.osL + (long long)ga * p.osA +
                               (long long)(gb + p.b_off) * p.osB;
-        epilogue_row<D, 128, EPI, DW / 8>(q, o, 1.0f / l_run, off, sQ + t * C::TILE_BYTES, row, hf * DW / 8);
+        epilogue_row_g<D, EPI, DW / 8>(q, o, 1.0f / l_run, off, in_off, hf * DW / 8);
       } else {
         const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
-        epilogue_row<D, 128, EPI, DW / 8>(p, o, 1.0f / l_run, off, sQ + t * C::TILE_BYTES, row, hf * DW / 8);
+        epilogue_row_g<D, EPI, DW / 8>(p, o, 1.0f / l_run, off, in_off, hf * DW / 8);
       }
     }
+    }  // items
+    if (PINGPONG && t == 0 && my_items > 0) named_bar_sync(1, 256 * SPLIT);  // consume tile 1's last turn
   } else {
     // ===================== converter warp (block temporal stage) =====================
     reg_dealloc<C::REG_PRODUCER>();
@@ -440,15 +482,18 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
       };
-      mbar_wait(q_full, 0);
-      convert_tile(sQ);
-      convert_tile(sQ + C::TILE_BYTES);
-      if (lane == 0) mbar_arrive(q_conv);
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j % NST;
-        mbar_wait(&k_full[s], (j / NST) & 1);
-        convert_tile(sKV + s * C::STAGE_BYTES);
-        if (lane == 0) mbar_arrive(&kv_conv[s]);
+      int g = 0;
+      for (int k = 0; k < my_items; ++k) {
+        mbar_wait(q_full, k & 1);
+        convert_tile(sQ);
+        convert_tile(sQ + C::TILE_BYTES);
+        if (lane == 0) mbar_arrive(q_conv);
+        for (int j = 0; j < nkv; ++j, ++g) {
+          const int s = g % NST;
+          mbar_wait(&k_full[s], (g / NST) & 1);
+          convert_tile(sKV + s * C::STAGE_BYTES);
+          if (lane == 0) mbar_arrive(&kv_conv[s]);
+        }
       }
     }
   }

@@ -205,8 +205,12 @@ static tsf_status launch_flash_emu(tsf_handle* h, cudaStream_t st, const CUtenso
                                    const CUtensorMap& mv, const AttnParams& p) {
   constexpr bool SH = EpiTraits<EPI>::SHARED;
   constexpr int NST = SH ? ((D == 128) ? 4 : 8) : ((D == 128) ? 2 : 4);
-  const long long grid = (long long)p.n_qpairs * p.A * p.B;
-  if (grid > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "grid too large");
+  const long long items = (long long)p.n_qpairs * p.A * p.B;
+  if (items > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "too many work items");
+  AttnParams pp = p;
+  pp.num_items = (int)items;
+  // persistent: one CTA per SM, each loops over work items
+  const long long grid = items < h->num_sms ? items : h->num_sms;
   static int split_env = -1, sub_env = -1;
   if (split_env < 0) {
     const char* e = getenv("TSF_SPLIT");
@@ -218,20 +222,20 @@ static tsf_status launch_flash_emu(tsf_handle* h, cudaStream_t st, const CUtenso
     if (split_env == 2) {
       if (sub_env == 64) {
         using C2 = FlashCfg<D, EPI, NST, 2, 64>;
-        return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 2, 64>, (int)grid, C2::THREADS, C2::SMEM, st, p, mq, mk,
+        return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 2, 64>, (int)grid, C2::THREADS, C2::SMEM, st, pp, mq, mk,
                       mv);
       }
       using C2 = FlashCfg<D, EPI, NST, 2, 128>;
-      return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 2, 128>, (int)grid, C2::THREADS, C2::SMEM, st, p, mq, mk,
+      return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 2, 128>, (int)grid, C2::THREADS, C2::SMEM, st, pp, mq, mk,
                     mv);
     }
   }
   if (sub_env == 64) {
     using C = FlashCfg<D, EPI, NST, 1, 64>;
-    return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 1, 64>, (int)grid, C::THREADS, C::SMEM, st, p, mq, mk, mv);
+    return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 1, 64>, (int)grid, C::THREADS, C::SMEM, st, pp, mq, mk, mv);
   }
   using C = FlashCfg<D, EPI, NST, 1, 128>;
-  return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 1, 128>, (int)grid, C::THREADS, C::SMEM, st, p, mq, mk, mv);
+  return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 1, 128>, (int)grid, C::THREADS, C::SMEM, st, pp, mq, mk, mv);
 }
 
 // exp2 emulation share (of 16) for the d = 64 flash kernel: TSF_EMU overrides
@@ -319,6 +323,7 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
   p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
   p.o = o;
   p.y = y;
+  p.res = q;  // the block's residual input (q = k = v there)
 #ifdef TSF_TRACE
   if (!h->trace) {
     cudaMalloc(&h->trace, 32 * TRACE_PER_WARP * sizeof(unsigned long long));
