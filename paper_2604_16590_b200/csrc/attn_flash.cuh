@@ -393,20 +393,26 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
       for (int c0 = 0; c0 < CW; c0 += 32) {
+        // three passes over 32 columns (scale, exponentiate, pack) so no
+        // MUFU result is consumed right after it is issued (in-order issue)
+        float xv[32], pv[32];
         uint32_t pk[16];
 #pragma unroll
-        for (int c = c0; c < c0 + 32; c += 2) {
-          float x0, x1, p0, p1;
-          ffma2(x0, x1, __uint_as_float(sv[c]), __uint_as_float(sv[c + 1]), sl2, sl2, nmb, nmb);
+        for (int c = 0; c < 32; c += 2)
+          ffma2(xv[c], xv[c + 1], __uint_as_float(sv[c0 + c]), __uint_as_float(sv[c0 + c + 1]), sl2, sl2, nmb, nmb);
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
           if (((c >> 1) & 7) >= 8 - EMU / 2) {
-            ex2_poly2(p0, p1, x0, x1);   // FMA/ALU pipes
-            pk[(c - c0) / 2] = pack2<F16>(p0, p1);
+            ex2_poly2(pv[c], pv[c + 1], xv[c], xv[c + 1]);   // FMA/ALU pipes
           } else {
-            p0 = ex2(x0);                // MUFU
-            p1 = ex2(x1);
-            pk[(c - c0) / 2] = pack2<F16>(p0, p1);
+            pv[c] = ex2(xv[c]);                              // MUFU
+            pv[c + 1] = ex2(xv[c + 1]);
           }
-          if constexpr (!C::ONES) { ls0 += p0; ls1 += p1; }
+        }
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          pk[c / 2] = pack2<F16>(pv[c], pv[c + 1]);
+          if constexpr (!C::ONES) { ls0 += pv[c]; ls1 += pv[c + 1]; }
         }
         tmem_st_x16(tSb + SUB / 2 + (c_off + c0) / 2, pk);
       }
