@@ -481,9 +481,31 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       constexpr int UPC = C::SWB / 16;
       const uint32_t ct = threadIdx.x - 32 * C::W_CONV;
       auto convert_tile = [&](uint8_t* tile) {
-        for (uint32_t i = ct; i < 128 * UPR; i += 32) {
-          const uint32_t row = i / UPR, u = i % UPR;
-          cvt_unit_bf16_to_f16(tile + (u / UPC) * C::CHUNK_BYTES + row * C::SWB + (u % UPC) * 16);
+        constexpr int PER = 128 * UPR / 32;   // units per lane (32 at d = 64)
+        constexpr int BATCH = 8;              // loads in flight per lane
+        static_assert(PER % BATCH == 0, "conversion batching");
+#pragma unroll 1
+        for (int b0 = 0; b0 < PER; b0 += BATCH) {
+          uint4 w[BATCH];
+          uint8_t* ptr[BATCH];
+#pragma unroll
+          for (int k = 0; k < BATCH; ++k) {
+            const uint32_t i = ct + 32 * (b0 + k);
+            const uint32_t row = i / UPR, u = i % UPR;
+            ptr[k] = tile + (u / UPC) * C::CHUNK_BYTES + row * C::SWB + (u % UPC) * 16;
+            w[k] = *reinterpret_cast<const uint4*>(ptr[k]);
+          }
+#pragma unroll
+          for (int k = 0; k < BATCH; ++k) {
+            uint32_t* q = reinterpret_cast<uint32_t*>(&w[k]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float lo = __uint_as_float(q[e] << 16), hi = __uint_as_float(q[e] & 0xFFFF0000u);
+              __half2 hv = __floats2half2_rn(lo, hi);
+              q[e] = *reinterpret_cast<uint32_t*>(&hv);
+            }
+            *reinterpret_cast<uint4*>(ptr[k]) = w[k];
+          }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
