@@ -206,3 +206,34 @@ def test_full_C2_block_every_row(tsf_lib):
     layer = tsf_lib.Layer(w.K, w.N, w.H, w.d)
     y = host(layer.block(to_dev(xb)))
     check(y, oracle.block(f64(xb)), "C2 block, all rows")
+
+
+@pytest.mark.parametrize("cfg,K", [("C3", 32), ("C4", 4)])
+def test_large_config_block_sampled(tsf_lib, cfg, K):
+    """C3 at full size; C4's shape (N=65536, H=16, d=128) at K=4 frames (one GPU)."""
+    w = synth.CONFIGS[cfg]
+    xb = synth.make_iid(K, w.N, w.H, w.d, seed=2)
+    layer = tsf_lib.Layer(K, w.N, w.H, w.d)
+    y = layer.block(to_dev(xb))
+    torch.cuda.synchronize()
+    x = f64(xb)
+    rows = sample_rows(K, w.N, w.H, 256, seed=13)
+    yi = torch.tensor(rows, dtype=torch.long)
+    got = y[yi[:, 0], yi[:, 1], yi[:, 2]].double().cpu().numpy()
+    check(got, oracle.block_rows(x, rows), f"{cfg} (K={K}) block sampled rows")
+
+
+def test_c_abi_program(tsf_lib, tmp_path):
+    """A plain C program against include/tsf.h and libtsf.so: create, block, destroy."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "tsf_c_smoke"
+    src = os.path.join(root, "tests", "c_abi_smoke.c")
+    libdir = os.path.join(root, "paper_2604_16590_b200")
+    r = subprocess.run(["gcc", "-O1", "-o", str(exe), src, "-I", os.path.join(root, "include"),
+                        "-I", "/usr/local/cuda/include", "-L", libdir, "-ltsf", f"-Wl,-rpath,{libdir}",
+                        "-L", "/usr/local/cuda/lib64", "-lcudart"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "C ABI OK" in r.stdout, r.stdout + r.stderr
