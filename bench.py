@@ -251,18 +251,26 @@ def main():
         torch.cuda.synchronize()
         barrier()
     ms = ev0.elapsed_time(ev1)
+    # per-stage event times of the timed steps only
+    st_ms = {s: layer.stage_ms(s) for s in (tsf.STAGE_TEMPORAL, tsf.STAGE_SPATIAL, tsf.STAGE_RESHARD)}
+    layer.set_timing(False)
+    if world > 1:
+        # every rank must run the same number of (collective) steps below
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_all = t.item()
+    else:
+        ms_all = ms
     if len(clk.lines) < 5:
         # timed region too short for nvidia-smi: sample clocks over a ~1 s
         # repeat of the same step loop (untimed)
-        reps = max(1, int(1000.0 / max(ms, 1e-3)))
+        reps = max(1, int(1000.0 / max(ms_all, 1e-3)))
         with ClockSampler(local) as clk:
             for _ in range(reps):
                 for i in range(args.steps):
                     layer.block(xs[i % R], out=ys[i % R])
             torch.cuda.synchronize()
         clk.note = f"sampled over a {reps}x repeat of the timed loop"
-    st_ms = {s: layer.stage_ms(s) for s in (tsf.STAGE_TEMPORAL, tsf.STAGE_SPATIAL, tsf.STAGE_RESHARD)}
-    layer.set_timing(False)
 
     # end to end through the C ABI with HOST buffers (pinned), copies timed
     xh = xs[0].cpu().pin_memory()
@@ -304,7 +312,7 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": dict(workload_config(K, N, H, d, world, args.config), l2_sets=R),
             "tflops": F / (step_ms / 1e3) / 1e12,
-            "tflops_frac_of_measured": F / (step_ms / 1e3) / 1e12 / pk["tflops"],
+            "tflops_frac_of_measured": F / (step_ms / 1e3) / 1e12 / (pk["tflops"] * world),
             "roofline": {"bound": "tensor", "kernel": f"attn_flash_kernel<{d}, EPI_BLOCK_S> (spatial stage)",
                          "achieved": achieved, "peak": pk["tflops"], "unit": "TFLOP/s",
                          "frac": achieved / pk["tflops"], "traffic": traffic_from_profiles(f"spatial_{args.config}"),
@@ -319,13 +327,19 @@ def main():
             "clocks": clocks,
         }
         if world > 1:
-            a2a_bytes = xs[0].numel() * 2            # X_t (fp16) bytes per rank entering the all-to-all
+            a2a_bytes = xs[0].numel() * 2            # X_t (fp16) bytes per rank entering the exchange
             rs_step_ms = rs_ms / args.steps
-            algbw = a2a_bytes / (rs_step_ms / 1e3) / 1e9
+            fused = layer.exchange_mode() == 2
             line["a2a"] = {"bytes_per_rank": a2a_bytes, "bytes_to_peers_per_rank": a2a_bytes * (world - 1) / world,
-                           "ms_per_step_comm_stream": rs_step_ms, "algbw_GBs": algbw,
-                           "busbw_GBs": algbw * (world - 1) / world, "nvlink_GBs_per_dir": 900,
-                           "overlap": "head-chunk pipeline: exchange(c+1) overlaps spatial(c)"}
+                           "ms_per_step_exchange_stage": rs_step_ms, "nvlink_GBs_per_dir": 900}
+            if fused:
+                line["a2a"]["mode"] = ("fused: the temporal kernel stores X_t rows into each rank's frame shard "
+                                       "over NVLink (CUDA IPC); the exchange stage is only the 1-int NCCL "
+                                       "all-reduce that orders the stores")
+            else:
+                algbw = a2a_bytes / (rs_step_ms / 1e3) / 1e9
+                line["a2a"].update(mode="NCCL grouped send/recv per head chunk; exchange(c+1) overlaps spatial(c)",
+                                   algbw_GBs=algbw, busbw_GBs=algbw * (world - 1) / world)
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(min(K, 8), N, H, d)
         print(json.dumps(line), flush=True)

@@ -126,6 +126,13 @@ const char* tsf_last_error(const tsf_handle* h);
 /* Number of kernels the last tsf_* compute call launched (bench accounting). */
 int tsf_last_launch_count(const tsf_handle* h);
 
+/* How a distributed handle moves X_t between the stages: 0 single GPU (no
+ * exchange), 1 NCCL grouped send/recv + unpack kernel, 2 fused NVLink scatter
+ * (the temporal kernel stores rows into every rank's frame shard through CUDA
+ * IPC mappings; a 1-int NCCL all-reduce orders the stores).  Shapes the fused
+ * scatter cannot tile use mode 1 per call.  Returns -1 for NULL. */
+int tsf_exchange_mode(const tsf_handle* h);
+
 /* Stage timing with CUDA events recorded on the call's stream around each
  * stage's kernel(s).  tsf_set_timing(h, 1) starts recording (clearing earlier
  * records), 0 stops.  tsf_stage_ms synchronises on the recorded events and

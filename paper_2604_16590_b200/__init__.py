@@ -46,6 +46,7 @@ SIGNATURES = [
     ("tsf_transpose", _I, [_P, _I, _I, _P, _P, _P]),
     ("tsf_last_error", ctypes.c_char_p, [_P]),
     ("tsf_last_launch_count", _I, [_P]),
+    ("tsf_exchange_mode", _I, [_P]),
     ("tsf_set_timing", _I, [_P, _I]),
     ("tsf_stage_ms", _I, [_P, _I, ctypes.POINTER(_F), ctypes.POINTER(_I)]),
 ]
@@ -223,6 +224,10 @@ class Layer:
     # ---- accounting ----
     def last_launch_count(self) -> int:
         return lib().tsf_last_launch_count(self._h)
+
+    def exchange_mode(self) -> int:
+        """0 single GPU, 1 NCCL send/recv + unpack, 2 fused NVLink scatter."""
+        return lib().tsf_exchange_mode(self._h)
 
     def set_timing(self, enable: bool):
         _check(lib().tsf_set_timing(self._h, 1 if enable else 0), self._h)

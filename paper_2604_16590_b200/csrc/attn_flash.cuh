@@ -45,9 +45,6 @@
 namespace tsf {
 
 constexpr float RESCALE_LOG2 = 8.0f;
-// Ping-pong of the two softmax warpgroups' exponential phases (named
-// barriers): measured slower at C2 (0.78 vs 0.75 ms), kept switchable.
-constexpr bool PINGPONG = true;
 
 // SPLIT = warps per tile row: 1, or 2 (d = 64: each warp of a pair takes 32 of
 // a sub-step's 64 columns, row maxima exchanged through shared memory) to put
@@ -220,8 +217,15 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
   } else if (warp == C::W_MMA0 || warp == C::W_MMA1) {
     // ===================== MMA issuers: one per query tile =====================
     reg_dealloc<C::REG_PRODUCER>();
-    const int t = warp - C::W_MMA0;
-    if (elect_one()) {
+    // FLASH_ONE_ISSUER: warp W_MMA0 issues both tiles in sub-step order
+    // (PV_0(i), S_0(i+LA), PV_1(i), S_1(i+LA)): the tensor pipe then finishes
+    // tile 0's work before tile 1's, which keeps the two softmax warpgroups
+    // half a period apart.  Otherwise one issuer per tile (their MMAs
+    // interleave in the pipe).
+    const bool one = (p.flags & FLASH_ONE_ISSUER) != 0;
+    const int t_self = warp - C::W_MMA0;
+    const int t_lo = one ? 0 : t_self, t_hi = one ? 1 : t_self;
+    if (!(one && t_self == 1) && elect_one()) {
       constexpr uint32_t idesc_qk = make_idesc(128, SUB, 0, 0, F16);
       constexpr uint32_t idesc_pv = make_idesc(128, C::OW, 0, 1, F16);
       constexpr uint32_t swz = (C::SWB == 128) ? SWZ_128B : SWZ_64B;
@@ -275,30 +279,33 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         else mbar_wait(q_full, k & 1);
         wait_k(g0);
         tc_fence_after();
-        for (int i = 0; i < LA && i < nsub; ++i) {
-          issue_s(t, i, G0 + i, g0);
-          if (i == nsub - 1) mma_commit(q_empty);   // Q no longer read once this retires
-        }
+        for (int i = 0; i < LA && i < nsub; ++i)
+          for (int t = t_lo; t <= t_hi; ++t) {
+            issue_s(t, i, G0 + i, g0);
+            if (i == nsub - 1) mma_commit(q_empty);   // Q no longer read once this retires
+          }
         for (int i = 0; i < nsub; ++i) {
           const int G = G0 + i, j = g0 + i / SPT;
           if (i % SPT == 0) wait_v(j);
           const bool last_of_tile = (i % SPT == SPT - 1) || i == nsub - 1;
           const bool more = i + LA < nsub;
           if (more && (i + LA) % SPT == 0) wait_k(g0 + (i + LA) / SPT);
-          mbar_wait(&p_full[2 * t + bufi(G)], phase(G));
-          TSF_STAMP(p, warp, 2 * i);
-          tc_fence_after();
-          if (i == 0 && k > 0) {  // the epilogue of the previous item has read O_t
-            mbar_wait(&o_empty[t], (k - 1) & 1);
+          for (int t = t_lo; t <= t_hi; ++t) {
+            mbar_wait(&p_full[2 * t + bufi(G)], phase(G));
+            TSF_STAMP(p, C::W_MMA0 + t, 2 * i);
             tc_fence_after();
+            if (i == 0 && k > 0) {  // the epilogue of the previous item has read O_t
+              mbar_wait(&o_empty[t], (k - 1) & 1);
+              tc_fence_after();
+            }
+            issue_pv(t, i, G, g0);
+            if (last_of_tile) mma_commit(&kv_empty[j % NST]);  // K_j/V_j free once both tiles' MMAs retire
+            if (more) {
+              issue_s(t, i + LA, G + LA, g0);  // reuses buffer b(G) after PV_t(G) (same issuer: in order)
+              if (i + LA == nsub - 1) mma_commit(q_empty);
+            }
+            TSF_STAMP(p, C::W_MMA0 + t, 2 * i + 1);
           }
-          issue_pv(t, i, G, g0);
-          if (last_of_tile) mma_commit(&kv_empty[j % NST]);  // K_j/V_j free once both tiles' MMAs retire
-          if (more) {
-            issue_s(t, i + LA, G + LA, g0);  // reuses buffer b(G) after PV_t(G) (same issuer: in order)
-            if (i + LA == nsub - 1) mma_commit(q_empty);
-          }
-          TSF_STAMP(p, warp, 2 * i + 1);
         }
       }
     }
@@ -315,6 +322,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     const uint32_t tSrow = tmem + lane_base + 128 * t;
     const uint32_t tOrow = tmem + lane_base + (t ? C::COL_O1 : C::COL_O0);
     const float sl2 = p.scale_log2;
+    const bool pingpong = (p.flags & FLASH_PINGPONG) != 0;
     int G0 = 0;
     for (int k = 0; k < my_items; ++k, G0 += nsub) {
     int qp, ga, gb;
@@ -388,8 +396,9 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       }
       // ping-pong: the two warpgroups take turns for the exponential phase
       // (MUFU-bound), so one's exps overlap the other's waits / max / stores
-      if (PINGPONG && !(t == 0 && G == 0)) named_bar_sync(1 + t, 256 * SPLIT);
-      const float nmb = -m_run;
+      if (pingpong && !(t == 0 && G == 0)) named_bar_sync(1 + t, 256 * SPLIT);
+      // every exponential depends on nmb: the fence keeps them below the barrier
+      const float nmb = reg_fence(-m_run);
       float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
       for (int c0 = 0; c0 < CW; c0 += 32) {
@@ -416,7 +425,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         }
         tmem_st_x16(tSb + SUB / 2 + (c_off + c0) / 2, pk);
       }
-      if (PINGPONG) named_bar_arrive(2 - t, 256 * SPLIT);
+      if (pingpong) named_bar_arrive(2 - t, 256 * SPLIT);
       float lsum = ls0 + ls1;
       if constexpr (SPLIT > 1 && !C::ONES) {
         // the row's other half: partial sums through the same parity slots
@@ -470,7 +479,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       }
     }
     }  // items
-    if (PINGPONG && t == 0 && my_items > 0) named_bar_sync(1, 256 * SPLIT);  // consume tile 1's last turn
+    if (pingpong && t == 0 && my_items > 0) named_bar_sync(1, 256 * SPLIT);  // consume tile 1's last turn
   } else {
     // ===================== converter warp (block temporal stage) =====================
     reg_dealloc<C::REG_PRODUCER>();

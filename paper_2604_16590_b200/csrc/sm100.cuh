@@ -104,6 +104,12 @@ TSF_DEV void reg_dealloc() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" 
 TSF_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// Register fence: the value is "redefined" by a volatile asm, so arithmetic
+// that consumes it cannot be scheduled above earlier volatile asm (barriers).
+TSF_DEV float reg_fence(float x) {
+  asm volatile("" : "+f"(x));
+  return x;
+}
 TSF_DEV void named_bar_arrive(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -211,13 +211,16 @@ static tsf_status launch_flash_emu(tsf_handle* h, cudaStream_t st, const CUtenso
   pp.num_items = (int)items;
   // persistent: one CTA per SM, each loops over work items
   const long long grid = items < h->num_sms ? items : h->num_sms;
-  static int split_env = -1, sub_env = -1;
+  static int split_env = -1, sub_env = -1, flags_env = -1;
   if (split_env < 0) {
     const char* e = getenv("TSF_SPLIT");
     split_env = e ? atoi(e) : 1;
     const char* f = getenv("TSF_SUB");
     sub_env = f ? atoi(f) : 128;
+    const char* g = getenv("TSF_FLASH_FLAGS");   // FLASH_ONE_ISSUER | FLASH_PINGPONG
+    flags_env = g ? atoi(g) : FLASH_PINGPONG;
   }
+  pp.flags = flags_env;
   if constexpr (D == 64) {
     if (split_env == 2) {
       if (sub_env == 64) {
@@ -584,6 +587,12 @@ void tsf_destroy(tsf_handle* h) {
 const char* tsf_last_error(const tsf_handle* h) { return h ? h->err.c_str() : g_create_err.c_str(); }
 
 int tsf_last_launch_count(const tsf_handle* h) { return h ? h->launches : 0; }
+
+int tsf_exchange_mode(const tsf_handle* h) {
+  if (!h) return -1;
+  if (h->world <= 1) return 0;
+  return h->fused ? 2 : 1;
+}
 
 tsf_status tsf_set_timing(tsf_handle* h, int enable) {
   if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
