@@ -75,12 +75,11 @@ struct AttnParams {
   // tensor, input-view strides): x (bf16) for EPI_BLOCK_T, X_t (fp16) for EPI_BLOCK_S
   const void* res;
   int num_items;  // flash kernel work items (pairs of query tiles x groups), persistent CTAs
-  // flash kernel schedule: FLASH_ONE_ISSUER (one MMA warp issues both query
-  // tiles' MMAs in sub-step order), FLASH_PINGPONG (softmax warpgroups take
+  // flash kernel schedule: FLASH_PINGPONG (the two softmax warpgroups take
   // turns for the exponential phase)
   int flags;
 };
-constexpr int FLASH_ONE_ISSUER = 1, FLASH_PINGPONG = 2;
+constexpr int FLASH_PINGPONG = 2;
 
 constexpr int MAX_PEERS = 8;
 // per-destination output tensor maps (packed kernel, distributed temporal stage)

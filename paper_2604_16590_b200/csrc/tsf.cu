@@ -200,8 +200,22 @@ static tsf_status launch_packed_t(tsf_handle* h, cudaStream_t st, const CUtensor
                 h->pm);
 }
 
-template <int D, int EPI, int EMU>
-static tsf_status launch_flash_emu(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
+// Flash kernel K/V tile rows (= score tile columns): d = 64 uses 96 (three
+// rotating score buffers fit TMEM next to O + l); otherwise 128.  TSF_SUB
+// (64 | 96 | 128) overrides for d = 64 experiments.
+static int flash_sub(int d) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("TSF_SUB");
+    env = e ? atoi(e) : -1;
+  }
+  if (d != 64) return 128;
+  if (env == 64 || env == 96 || env == 128) return env;
+  return 96;
+}
+
+template <int D, int EPI, int EMU, int SUB>
+static tsf_status launch_flash_sub(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
                                    const CUtensorMap& mv, const AttnParams& p) {
   constexpr bool SH = EpiTraits<EPI>::SHARED;
   constexpr int NST = SH ? ((D == 128) ? 4 : 8) : ((D == 128) ? 2 : 4);
@@ -209,36 +223,29 @@ static tsf_status launch_flash_emu(tsf_handle* h, cudaStream_t st, const CUtenso
   if (items > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "too many work items");
   AttnParams pp = p;
   pp.num_items = (int)items;
-  // persistent: one CTA per SM, each loops over work items
-  const long long grid = items < h->num_sms ? items : h->num_sms;
-  static int split_env = -1, sub_env = -1, flags_env = -1;
-  if (split_env < 0) {
-    const char* e = getenv("TSF_SPLIT");
-    split_env = e ? atoi(e) : 1;
-    const char* f = getenv("TSF_SUB");
-    sub_env = f ? atoi(f) : 128;
-    const char* g = getenv("TSF_FLASH_FLAGS");   // FLASH_ONE_ISSUER | FLASH_PINGPONG
-    flags_env = g ? atoi(g) : FLASH_PINGPONG;
+  static int flags_env = -1;
+  if (flags_env < 0) {
+    const char* g = getenv("TSF_FLASH_FLAGS");  // FLASH_PINGPONG (off: measured slower with rotating buffers)
+    flags_env = g ? atoi(g) : 0;
   }
   pp.flags = flags_env;
+  // persistent: one CTA per SM, each loops over work items
+  const long long grid = items < h->num_sms ? items : h->num_sms;
+  using C = FlashCfg<D, EPI, NST, SUB>;
+  return launch(h, attn_flash_kernel<D, EPI, NST, EMU, SUB>, (int)grid, C::THREADS, C::SMEM, st, pp, mq, mk, mv);
+}
+
+template <int D, int EPI, int EMU>
+static tsf_status launch_flash_emu(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
+                                   const CUtensorMap& mv, const AttnParams& p) {
   if constexpr (D == 64) {
-    if (split_env == 2) {
-      if (sub_env == 64) {
-        using C2 = FlashCfg<D, EPI, NST, 2, 64>;
-        return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 2, 64>, (int)grid, C2::THREADS, C2::SMEM, st, pp, mq, mk,
-                      mv);
-      }
-      using C2 = FlashCfg<D, EPI, NST, 2, 128>;
-      return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 2, 128>, (int)grid, C2::THREADS, C2::SMEM, st, pp, mq, mk,
-                    mv);
+    switch (flash_sub(D)) {
+      case 64: return launch_flash_sub<D, EPI, EMU, 64>(h, st, mq, mk, mv, p);
+      case 128: return launch_flash_sub<D, EPI, EMU, 128>(h, st, mq, mk, mv, p);
+      default: return launch_flash_sub<D, EPI, EMU, 96>(h, st, mq, mk, mv, p);
     }
   }
-  if (sub_env == 64) {
-    using C = FlashCfg<D, EPI, NST, 1, 64>;
-    return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 1, 64>, (int)grid, C::THREADS, C::SMEM, st, pp, mq, mk, mv);
-  }
-  using C = FlashCfg<D, EPI, NST, 1, 128>;
-  return launch(h, attn_flash_kernel<D, EPI, NST, EMU, 1, 128>, (int)grid, C::THREADS, C::SMEM, st, pp, mq, mk, mv);
+  return launch_flash_sub<D, EPI, EMU, 128>(h, st, mq, mk, mv, p);
 }
 
 // exp2 emulation share (of 16) for the d = 64 flash kernel: TSF_EMU overrides
@@ -261,7 +268,6 @@ static tsf_status launch_flash_t(tsf_handle* h, cudaStream_t st, const CUtensorM
                                  const CUtensorMap& mv, const AttnParams& p) {
   if constexpr (D == 64) {
     switch (emu_setting(D, EPI)) {
-      case 2: return launch_flash_emu<D, EPI, 2>(h, st, mq, mk, mv, p);
       case 4: return launch_flash_emu<D, EPI, 4>(h, st, mq, mk, mv, p);
       case 6: return launch_flash_emu<D, EPI, 6>(h, st, mq, mk, mv, p);
       case 8: return launch_flash_emu<D, EPI, 8>(h, st, mq, mk, mv, p);
@@ -373,10 +379,11 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
     }
   } else {
     p.n_qpairs = (v.L + 255) / 256;
-    p.nkv = (v.L + 127) / 128;
+    const int sub = flash_sub(d);  // K/V tile rows
+    p.nkv = (v.L + sub - 1) / sub;
     if ((s = make_map(h, &mq, q, d, v, 128, 1, 1, f16)) != TSF_OK) return s;
-    if ((s = make_map(h, &mk, k, d, v, 128, 1, 1, f16)) != TSF_OK) return s;
-    if ((s = make_map(h, &mv, vv, d, v, 128, 1, 1, f16)) != TSF_OK) return s;
+    if ((s = make_map(h, &mk, k, d, v, sub, 1, 1, f16)) != TSF_OK) return s;
+    if ((s = make_map(h, &mv, vv, d, v, sub, 1, 1, f16)) != TSF_OK) return s;
   }
   switch (d) {
     case 32: return dispatch_d<32>(h, packed, win, epi, st, mq, mk, mv, mo, p);

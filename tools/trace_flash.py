@@ -5,7 +5,7 @@
 
 Softmax warp stamps per sub-step i: 0 loop top, 1 S ready (s_full), 2 S in
 registers, 3 row max done, 4 P stored, 5 p_full arrived.  MMA warp (9): per
-sub-step i and tile t: 4i+2t p_full seen, 4i+2t+1 PV(i) and S(i+2) issued.
+score tile n = 2i + t: 2n p_full seen, 2n+1 PV(n) and S(n + NB) issued.
 """
 import ctypes
 import os
@@ -39,7 +39,7 @@ def main():
     torch.cuda.synchronize()
     L.tsf_trace_read(layer._h, buf, 16 * PER_WARP)
     a = np.frombuffer(buf, dtype=np.uint64).reshape(16, PER_WARP).astype(np.int64)
-    sub = int(os.environ.get("TSF_SUB", "128"))
+    sub = int(os.environ.get("TSF_SUB", "96" if d == 64 else "128"))
     nsub = (N + sub - 1) // sub
     t0 = a[a > 0].min()
     print(f"{what} TSF_EMU={os.environ.get('TSF_EMU', 'default')} nsub={nsub}  kernel span (CTA0 stamps) {a.max() - t0} cycles")
@@ -51,14 +51,13 @@ def main():
         per = dif.mean(0).tolist() + [nxt.mean()]
         tot = (s[-1, 5] - s[0, 0]) / nsub
         print(f"warp {w}: cycles/sub-step {tot:7.1f} | " + " ".join(f"{p} {v:6.1f}" for p, v in zip(phases, per)))
-    for w in (9, 10):
-        m = a[w, :2 * nsub].reshape(nsub, 2)
-        print(f"MMA warp {w}: mean cycles p_full->issued {np.diff(m, axis=1).mean():.1f}, "
-              f"issued->next p_full {(m[1:, 0] - m[:-1, 1]).mean():.1f}")
+    m = a[9, :4 * nsub].reshape(2 * nsub, 2)
+    print(f"MMA warp 9: mean cycles p_full->issued {np.diff(m, axis=1).mean():.1f}, "
+          f"issued->next p_full {(m[1:, 0] - m[:-1, 1]).mean():.1f}")
     print("first sub-steps, warp 0 and warp 4 (relative to kernel start):")
     for i in range(min(6, nsub)):
         print(i, (a[0, 6 * i:6 * i + 6] - t0).tolist(), (a[4, 6 * i:6 * i + 6] - t0).tolist(),
-              (a[9, 2 * i:2 * i + 2] - t0).tolist(), (a[10, 2 * i:2 * i + 2] - t0).tolist())
+              (a[9, 4 * i:4 * i + 4] - t0).tolist())
     os.makedirs("gpurun_out", exist_ok=True)
     np.save("gpurun_out/trace_flash.npy", a)
 

@@ -4,7 +4,7 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out/var
 # VARIANTS="sub,split,emu,flags ..."
-for v in ${VARIANTS:-128,1,4,2 128,1,4,3 128,1,4,1 128,1,4,0}; do
+for v in ${VARIANTS:-96,1,4,0 96,1,6,0 96,1,8,0 96,1,6,2 64,1,4,0}; do
   set -- ${v//,/ }
   fl=${4:-2}
   tag="$1_$2_$3_$fl"
