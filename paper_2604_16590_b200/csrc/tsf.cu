@@ -48,9 +48,16 @@ struct tsf_handle {
   int nchunk = 1;
   cudaStream_t comm_stream = nullptr;
   std::vector<cudaEvent_t> ev_t, ev_a;
-  // fused exchange: every rank's frame-shard X_t buffer (uxt) mapped here
-  // through CUDA IPC; the temporal kernel stores X_t rows straight into them
-  void* peer_uxt[MAX_PEERS] = {};
+  // fused exchange: every rank's frame-shard X_t buffers mapped here through
+  // CUDA IPC; the temporal kernel stores X_t rows straight into them.  Two
+  // buffers used on alternate calls (ubuf[0] = uxt): a rank's next temporal
+  // stage may write a peer's buffer while that peer's spatial stage still
+  // reads the other one; the all-reduce of the call in between orders reuse.
+  __half* ubuf[2] = {};
+  void* peer_buf[2][MAX_PEERS] = {};
+  int fparity = 0;
+  int fchunks = 1;                       // head chunks of the fused pipeline (TSF_FUSED_CHUNKS)
+  std::vector<cudaEvent_t> ev_f;         // [fchunks + 1]
   bool fused = false;
   int* d_flag = nullptr;        // 1-int NCCL all-reduce = cross-rank barrier
   PeerMaps pm{};                // per-destination output maps of the current launch
@@ -60,6 +67,7 @@ struct tsf_handle {
 // Output routing of the distributed temporal stage (run_attention).
 struct DistOut {
   int P, Kc, rank, Nl;
+  void* const* peers;   // every rank's frame-shard buffer (this call's parity, head-chunk offset applied)
 };
 
 static thread_local std::string g_create_err;
@@ -324,7 +332,7 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
     p.P = dist->P;
     p.Kc = dist->Kc;
     p.b_off = dist->rank * dist->Nl;
-    for (int r = 0; r < dist->P; ++r) p.peer_out[r] = h->peer_uxt[r];
+    for (int r = 0; r < dist->P; ++r) p.peer_out[r] = dist->peers[r];
     p.osL = (long long)h->N * h->H * h->d;
     p.osA = h->d;
     p.osB = (long long)h->H * h->d;
@@ -372,7 +380,7 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
         return fail(h, TSF_ERR_UNSUPPORTED, "fused exchange needs (K/P) * groups-per-tile % 8 == 0");
       for (int r = 0; r < dist->P; ++r) {
         const View pv{dist->Kc, v.A, dist->Nl, p.osL, p.osA, p.osB};
-        const void* base = static_cast<const __half*>(h->peer_uxt[r]) + (size_t)dist->rank * dist->Nl * h->H * d;
+        const void* base = static_cast<const __half*>(dist->peers[r]) + (size_t)dist->rank * dist->Nl * h->H * d;
         if ((s = make_map(h, &h->pm.m[r], base, d, pv, dist->Kc, Ab, Bb, true)) != TSF_OK) return s;
       }
       h->use_pm = true;
@@ -532,24 +540,37 @@ tsf_status tsf_create_dist(int K, int N, int H, int d, const void* id128, int ra
       cudaEventCreateWithFlags(&h->ev_t[c], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&h->ev_a[c], cudaEventDisableTiming);
     }
-    // fused exchange: all-gather the IPC handles of every rank's uxt and map them
+    // fused exchange: all-gather the IPC handles of every rank's two frame-shard
+    // X_t buffers and map them
     const char* fe = getenv("TSF_FUSED_EXCHANGE");
     if (world <= MAX_PEERS && !(fe && atoi(fe) == 0)) {
-      cudaIpcMemHandle_t mine;
+      const size_t El = (size_t)h->K * (h->N / world) * h->H * h->d;
+      h->ubuf[0] = h->uxt;
+      cudaIpcMemHandle_t mine[2];
       char* dh = nullptr;
-      bool ok = cudaIpcGetMemHandle(&mine, h->uxt) == cudaSuccess &&
+      bool ok = cudaMalloc(reinterpret_cast<void**>(&h->ubuf[1]), El * sizeof(__half)) == cudaSuccess &&
+                cudaIpcGetMemHandle(&mine[0], h->ubuf[0]) == cudaSuccess &&
+                cudaIpcGetMemHandle(&mine[1], h->ubuf[1]) == cudaSuccess &&
                 cudaMalloc(&dh, (size_t)world * sizeof mine) == cudaSuccess &&
                 cudaMalloc(&h->d_flag, sizeof(int)) == cudaSuccess &&
-                cudaMemcpy(dh + rank * sizeof mine, &mine, sizeof mine, cudaMemcpyHostToDevice) == cudaSuccess;
-      std::vector<cudaIpcMemHandle_t> all(world);
+                cudaMemcpy(dh + rank * sizeof mine, mine, sizeof mine, cudaMemcpyHostToDevice) == cudaSuccess;
+      std::vector<cudaIpcMemHandle_t> all(2 * world);
       if (ok) ok = ncclAllGather(dh + rank * sizeof mine, dh, sizeof mine, ncclUint8, h->comm, h->comm_stream) ==
                    ncclSuccess &&
                    cudaStreamSynchronize(h->comm_stream) == cudaSuccess &&
                    cudaMemcpy(all.data(), dh, (size_t)world * sizeof mine, cudaMemcpyDeviceToHost) == cudaSuccess;
-      for (int p = 0; ok && p < world; ++p) {
-        if (p == rank) h->peer_uxt[p] = h->uxt;
-        else ok = cudaIpcOpenMemHandle(&h->peer_uxt[p], all[p], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
-      }
+      for (int p = 0; ok && p < world; ++p)
+        for (int b = 0; ok && b < 2; ++b) {
+          if (p == rank) h->peer_buf[b][p] = h->ubuf[b];
+          else ok = cudaIpcOpenMemHandle(&h->peer_buf[b][p], all[2 * p + b], cudaIpcMemLazyEnablePeerAccess) ==
+                    cudaSuccess;
+        }
+      int fc = 1;
+      if (const char* e = getenv("TSF_FUSED_CHUNKS")) fc = atoi(e);
+      if (fc < 1 || h->H % fc) fc = 1;
+      h->fchunks = fc;
+      h->ev_f.resize(fc + 1);
+      for (auto& e : h->ev_f) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
       if (dh) cudaFree(dh);
       cudaGetLastError();
       // every rank must agree on the mode: all-reduce (min) of the local outcome
@@ -579,8 +600,11 @@ void tsf_destroy(tsf_handle* h) {
     else ncclCommDestroy(h->comm);
   }
   for (auto& r : h->recs) { cudaEventDestroy(r.e0); cudaEventDestroy(r.e1); }
-  for (int p = 0; p < h->world && p < MAX_PEERS; ++p)
-    if (h->peer_uxt[p] && h->peer_uxt[p] != h->uxt) cudaIpcCloseMemHandle(h->peer_uxt[p]);
+  for (int b = 0; b < 2; ++b)
+    for (int p = 0; p < h->world && p < MAX_PEERS; ++p)
+      if (h->peer_buf[b][p] && p != h->rank) cudaIpcCloseMemHandle(h->peer_buf[b][p]);
+  if (h->ubuf[1]) cudaFree(h->ubuf[1]);
+  for (auto e : h->ev_f) cudaEventDestroy(e);
   if (h->d_flag) cudaFree(h->d_flag);
   for (auto e : h->ev_t) cudaEventDestroy(e);
   for (auto e : h->ev_a) cudaEventDestroy(e);
@@ -716,23 +740,73 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
     // Fused exchange: the temporal kernel writes X_t rows straight into the
     // owning rank's frame shard (CUDA IPC + NVLink TMA/plain stores), a 1-int
     // NCCL all-reduce orders every rank's stores before any spatial read.
-    const DistOut dist{P, Kl, h->rank, Nl};
-    {
-      StageTimer tm(h, st, 0);
-      s = run_attention(h, temporal_view(h->K, Nl, h->H, h->d), x, x, x, EPI_BLOCK_T, nullptr, nullptr, st,
-                        nullptr, &dist);
-      tm.done();
+    // With fchunks > 1 the heads are split into chunks: temporal(c) + its
+    // all-reduce run on the comm stream, spatial(c) on `st` after them, so the
+    // NVLink stores of chunk c+1 overlap the spatial stage of chunk c.
+    const int par = h->fparity, nc = h->fchunks, H = h->H, d = h->d, Hc = H / nc;
+    const __half* u = h->ubuf[par];
+    auto peers_of = [&](int c, void** out) {
+      for (int r = 0; r < P; ++r) out[r] = static_cast<__half*>(h->peer_buf[par][r]) + (size_t)c * Hc * d;
+    };
+    if (nc == 1) {
+      void* peers[MAX_PEERS];
+      peers_of(0, peers);
+      const DistOut dist{P, Kl, h->rank, Nl, peers};
+      {
+        StageTimer tm(h, st, 0);
+        s = run_attention(h, temporal_view(h->K, Nl, H, d), x, x, x, EPI_BLOCK_T, nullptr, nullptr, st, nullptr,
+                          &dist);
+        tm.done();
+      }
+      if (s == TSF_OK) {
+        StageTimer tm(h, st, 2);
+        TSF_NCCL(h, ncclAllReduce(h->d_flag, h->d_flag, 1, ncclInt32, ncclSum, h->comm, st));
+        tm.done();
+        StageTimer tm1(h, st, 1);
+        s = run_attention(h, spatial_view(Kl, h->N, H, d), u, u, u, EPI_BLOCK_S, nullptr, y, st);
+        tm1.done();
+        if (s == TSF_OK) h->fparity ^= 1;
+        return s;
+      }
+      if (s != TSF_ERR_UNSUPPORTED) return s;
+    } else {
+      cudaStream_t cs = h->comm_stream;
+      TSF_CUDA(h, cudaEventRecord(h->ev_f[nc], st));  // x ready
+      TSF_CUDA(h, cudaStreamWaitEvent(cs, h->ev_f[nc], 0));
+      const View vin{h->K, Hc, Nl, (long long)Nl * H * d, (long long)d, (long long)H * d};
+      for (int c = 0; c < nc && s == TSF_OK; ++c) {
+        void* peers[MAX_PEERS];
+        peers_of(c, peers);
+        const DistOut dist{P, Kl, h->rank, Nl, peers};
+        const tsf_bf16* xc = x + (size_t)c * Hc * d;
+        {
+          StageTimer tm(h, cs, 0);
+          s = run_attention(h, vin, xc, xc, xc, EPI_BLOCK_T, nullptr, nullptr, cs, nullptr, &dist);
+          tm.done();
+        }
+        if (s != TSF_OK) break;
+        StageTimer tm(h, cs, 2);
+        TSF_NCCL(h, ncclAllReduce(h->d_flag, h->d_flag, 1, ncclInt32, ncclSum, h->comm, cs));
+        tm.done();
+        TSF_CUDA(h, cudaEventRecord(h->ev_f[c], cs));
+      }
+      if (s == TSF_OK) {
+        const View vs{h->N, Hc, Kl, (long long)H * d, (long long)d, (long long)h->N * H * d};
+        for (int c = 0; c < nc && s == TSF_OK; ++c) {
+          TSF_CUDA(h, cudaStreamWaitEvent(st, h->ev_f[c], 0));
+          StageTimer tm(h, st, 1);
+          const __half* uc = u + (size_t)c * Hc * d;
+          s = run_attention(h, vs, uc, uc, uc, EPI_BLOCK_S, nullptr, y + (size_t)c * Hc * d, st, &vs);
+          tm.done();
+        }
+        if (s == TSF_OK) h->fparity ^= 1;
+        return s;
+      }
+      // the comm stream must not run ahead of a fallback on `st`
+      TSF_CUDA(h, cudaEventRecord(h->ev_f[nc], cs));
+      TSF_CUDA(h, cudaStreamWaitEvent(st, h->ev_f[nc], 0));
+      if (s != TSF_ERR_UNSUPPORTED) return s;
     }
-    if (s == TSF_OK) {
-      StageTimer tm(h, st, 2);
-      TSF_NCCL(h, ncclAllReduce(h->d_flag, h->d_flag, 1, ncclInt32, ncclSum, h->comm, st));
-      tm.done();
-      StageTimer tm1(h, st, 1);
-      s = run_attention(h, spatial_view(Kl, h->N, h->H, h->d), h->uxt, h->uxt, h->uxt, EPI_BLOCK_S, nullptr, y, st);
-      tm1.done();
-      return s;
-    }
-    if (s != TSF_ERR_UNSUPPORTED) return s;
     // shapes the fused scatter cannot tile: fall through to the NCCL path
   }
   // Distributed: head-chunk pipeline.  temporal(c) for all chunks on `st`;

@@ -45,6 +45,18 @@ def main():
     plane = y[0, :, 0].double().cpu().numpy()
     perr = np.abs(plane - oracle.block_plane(x, rank * Kl, 0)).max()
 
+    # back-to-back calls (no host sync) with alternating inputs: every call's
+    # output must equal the isolated call's output bitwise (buffer reuse hazards)
+    xs2 = torch.flip(xs, dims=[0]).contiguous()
+    y2_ref = layer.block(xs2).clone()
+    torch.cuda.synchronize()
+    dist.barrier()
+    outs = []
+    for it in range(6):
+        outs.append(layer.block(xs if it % 2 == 0 else xs2).clone())
+    torch.cuda.synchronize()
+    b2b = all(torch.equal(o, y if it % 2 == 0 else y2_ref) for it, o in enumerate(outs))
+
     # reshard round trip, bit-exact
     fr = layer.reshard(xs, tsf.TSF_T2S)
     back = layer.reshard(fr, tsf.TSF_S2T)
@@ -61,8 +73,9 @@ def main():
         same = torch.equal(y1[:Kl], y)
         single.close()
     print(f"rank {rank}/{world}: block sampled max-abs {err:.3e}, plane max-abs {perr:.3e}, "
-          f"t2s exact {exact_fr}, round trip exact {exact_back}, equals single-GPU bitwise {same}", flush=True)
-    ok = err <= 2e-2 and perr <= 2e-2 and exact_fr and exact_back and (same in (None, True))
+          f"t2s exact {exact_fr}, round trip exact {exact_back}, back-to-back bitwise {b2b}, "
+          f"equals single-GPU bitwise {same}", flush=True)
+    ok = err <= 2e-2 and perr <= 2e-2 and exact_fr and exact_back and b2b and (same in (None, True))
     flag = torch.tensor([0 if ok else 1], device="cuda")
     dist.all_reduce(flag)
     layer.close()
