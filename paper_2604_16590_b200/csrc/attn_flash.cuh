@@ -47,7 +47,7 @@ namespace tsf {
 
 constexpr float RESCALE_LOG2 = 8.0f;
 
-template <int D, int EPI, int NST, int SUB>
+template <int D, int EPI, int NST, int SUB, int SPLIT_ = 1>
 struct FlashCfg {
   static constexpr int SWB = (2 * D < 128) ? 2 * D : 128;  // bytes per swizzled row chunk
   static constexpr int CH = SWB / 2;                       // 16-bit elements per chunk row
@@ -61,51 +61,78 @@ struct FlashCfg {
   static constexpr int STAGE_BYTES = (SHARED ? 1 : 2) * KV_TILE;
   static constexpr bool ONES = (D == 64);
   static constexpr int ONES_BYTES = ONES ? SUB * SWB : 0;
-  static constexpr int SMEM = Q_BYTES + NST * STAGE_BYTES + ONES_BYTES + 1024 + 256;
+  static constexpr uint32_t OW = ONES ? D + 16 : D;
+  // SEP: each query tile owns an S buffer (SUB fp32 columns) and a separate P
+  // buffer (SUB / 2 columns of 16-bit pairs).  The softmax releases S as soon
+  // as it has loaded it, so S_t(g+1) is computed while the softmax of S_t(g)
+  // is still exponentiating.  Needs 2 OW + 3 SUB <= 512 TMEM columns (d = 32,
+  // 64); d = 128 uses rotating S/P buffers instead (below).
+  static constexpr bool SEP = (2 * (int)OW + 3 * SUB) <= 512;
+  // SPLIT = 2: two softmax warps per tile row group, each owning half of the
+  // score columns (row maxima exchanged through shared memory), i.e. four
+  // softmax warps per SM sub-partition to keep MUFU busy.  Needs SEP and the
+  // ones-column denominator (no partial row sums to combine).
+  static constexpr int SPLIT = SPLIT_;
+  static_assert(SPLIT == 1 || (SPLIT == 2 && SEP && ONES), "SPLIT = 2 needs SEP and d = 64");
+  static constexpr int CW = SUB / SPLIT;                   // score columns per softmax warp
+  static_assert(CW % 16 == 0, "columns per warp");
+  static constexpr int QST = SEP ? 2 : 1;                  // Q stages (double-buffered when SMEM allows)
+  static constexpr int XMAX_BYTES = SPLIT > 1 ? 2 * 2 * SPLIT * 128 * 4 : 0;  // [parity][tile][half][row]
+  static constexpr int BAR_BYTES = 1024;
+  static constexpr int SMEM = QST * Q_BYTES + NST * STAGE_BYTES + ONES_BYTES + XMAX_BYTES + BAR_BYTES + 1024;
   static_assert(SMEM <= 227 * 1024, "shared memory");
   static_assert(SUB % 32 == 0 && SUB >= 64 && SUB <= 128, "KV tile rows");
-  static constexpr uint32_t OW = ONES ? D + 16 : D;
   static constexpr uint32_t COL_O0 = 0, COL_O1 = OW, COL_S = 2 * OW;
+  static constexpr uint32_t COL_P = 2 * OW + 2 * SUB;      // SEP: P_0 | P_1 after S_0 | S_1
   // rotating score buffers, at most 3: the rescale of O_t at S_t(g) waits for
   // PV_t(g-1) on o_full[t] by parity, which needs PV_t(g-2) retired; S(m)
   // is issued after PV(m - NB), which implies that only for NB <= 3
   static constexpr int NB_FIT = (512 - 2 * (int)OW) / SUB;
-  static constexpr int NB = NB_FIT < 3 ? NB_FIT : 3;
+  static constexpr int NB = SEP ? 2 : (NB_FIT < 3 ? NB_FIT : 3);
   static_assert(NB >= 2, "TMEM budget");
-  static constexpr int W_TMA = 8, W_MMA = 9, W_CONV = 11;
-  static constexpr int THREADS = 384;                       // whole warpgroups (setmaxnreg is per warpgroup)
-  // setmaxnreg must balance: (168 - 56) x 128 released >= (224 - 168) x 256 gained
-  static constexpr int REG_SOFTMAX = 224, REG_PRODUCER = 56;
+  static constexpr int NSOFT = 8 * SPLIT;                   // softmax warps: tile t = w / (4 SPLIT)
+  static constexpr int W_TMA = NSOFT, W_MMA = NSOFT + 1, W_CONV = NSOFT + 3;
+  static constexpr int THREADS = 32 * (NSOFT + 4);          // whole warpgroups (setmaxnreg is per warpgroup)
+  // setmaxnreg must balance within the launch allocation (65536 / THREADS,
+  // rounded down to 8): SPLIT 1: 168 -> 224 / 56; SPLIT 2: 96 -> 104 / 48
+  static constexpr int REG_SOFTMAX = SPLIT == 1 ? 224 : 104, REG_PRODUCER = SPLIT == 1 ? 56 : 48;
 };
 
-template <int D, int EPI, int NST, int EMU, int SUB>
-__global__ void __launch_bounds__(384, 1)
+template <int D, int EPI, int NST, int EMU, int SUB, int SPLIT>
+__global__ void __launch_bounds__(FlashCfg<D, EPI, NST, SUB, SPLIT>::THREADS, 1)
 attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                   const __grid_constant__ CUtensorMap tv, const AttnParams p) {
-  using C = FlashCfg<D, EPI, NST, SUB>;
+  using C = FlashCfg<D, EPI, NST, SUB, SPLIT>;
   constexpr int NB = C::NB;
   constexpr bool F16 = EpiTraits<EPI>::F16;
   constexpr bool CONVERT = EpiTraits<EPI>::CONVERT;
   constexpr bool SHARED = C::SHARED;
+  // block spatial stage: the residual X_t row is the query row itself (q = X_t),
+  // so the epilogue reads it from the Q tile in shared memory (Q double-buffered)
+  constexpr bool RES_SMEM_OK = C::SEP && EPI == EPI_BLOCK_S;
+  const bool RES_SMEM = RES_SMEM_OK && !(p.flags & 4);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                        // Q0 | Q1
-  uint8_t* sKV = smem + C::Q_BYTES;          // NST x (K | V)
+  uint8_t* sQ = smem;                        // QST x (Q0 | Q1)
+  uint8_t* sKV = smem + C::QST * C::Q_BYTES; // NST x (K | V)
   uint8_t* sOnes = sKV + NST * C::STAGE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;               // [NST]
+  float* xmax = reinterpret_cast<float*>(sOnes + C::ONES_BYTES);  // SPLIT > 1: [2][2][SPLIT][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES + C::XMAX_BYTES);
+  uint64_t* q_full = bars;                   // [QST]
+  uint64_t* k_full = bars + C::QST;          // [NST]
   uint64_t* v_full = k_full + NST;           // [NST]
   uint64_t* kv_empty = v_full + NST;         // [NST]
   uint64_t* kv_conv = kv_empty + NST;        // [NST] converter -> MMA (CONVERT only)
   uint64_t* s_full = kv_conv + NST;          // [NB] score buffer written (MMA commit)
   uint64_t* p_full = s_full + NB;            // [NB] P stored (4 softmax warps)
-  uint64_t* o_full = p_full + NB;            // [2] one phase per PV of the tile
+  uint64_t* s_free = p_full + NB;            // [2] SEP: S_t loaded into registers (4 softmax warps)
+  uint64_t* o_full = s_free + 2;             // [2] one phase per PV of the tile
   uint64_t* o_done = o_full + 2;             // [2] last PV of the item retired (one phase per item)
   uint64_t* o_empty = o_done + 2;            // [2] epilogue read O -> next item's PV may overwrite
-  uint64_t* q_empty = o_empty + 2;           // last QK^T of the item retired -> next Q may load
-  uint64_t* q_conv = q_empty + 1;            // converter warp -> MMA (CONVERT only)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(q_conv + 1);
+  uint64_t* q_empty = o_empty + 2;           // [QST] last QK^T of the item retired -> next Q may load
+  uint64_t* q_conv = q_empty + C::QST;       // [QST] converter warp -> MMA (CONVERT only)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(q_conv + C::QST);
+  static_assert(sizeof(uint64_t) * (3 * C::QST + 4 * NST + 2 * NB + 8) + 4 <= C::BAR_BYTES, "barrier space");
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int L = p.L, nkv = p.nkv;  // nkv = ceil(L / SUB) KV tiles per group
@@ -128,24 +155,27 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
+    for (int q = 0; q < C::QST; ++q) {
+      mbar_init(&q_full[q], 1);
+      mbar_init(&q_conv[q], 1);
+      mbar_init(&q_empty[q], 2 + (RES_SMEM ? C::NSOFT : 0));  // last S of both tiles (+ every softmax warp's epilogue)
+    }
     for (int s = 0; s < NST; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
       mbar_init(&kv_empty[s], 2);  // one commit after each query tile's PV
       mbar_init(&kv_conv[s], 1);
     }
-    mbar_init(q_conv, 1);
     for (int b = 0; b < NB; ++b) {
       mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], 4);
+      mbar_init(&p_full[b], 4 * SPLIT);
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&o_full[t], 1);
       mbar_init(&o_done[t], 1);
-      mbar_init(&o_empty[t], 4);
+      mbar_init(&o_empty[t], 4 * SPLIT);
+      mbar_init(&s_free[t], 4 * SPLIT);
     }
-    mbar_init(q_empty, 2);
     fence_barrier_init();
   }
   if (warp == C::W_MMA) tmem_alloc<512>(tmem_holder);
@@ -167,13 +197,15 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       for (int k = 0; k < my_items; ++k) {
         int qp, ga, gb;
         item_coords(k, qp, ga, gb);
-        if (k > 0) mbar_wait_sleep(q_empty, (k - 1) & 1);
-        mbar_arrive_expect_tx(q_full, C::Q_BYTES);
+        const int qs = k % C::QST;
+        if (k >= C::QST) mbar_wait_sleep(&q_empty[qs], ((k / C::QST) - 1) & 1);
+        mbar_arrive_expect_tx(&q_full[qs], C::Q_BYTES);
 #pragma unroll
         for (int t = 0; t < 2; ++t)
 #pragma unroll
           for (int c = 0; c < C::NCH; ++c)
-            tma_load_4d(sQ + t * C::Q_TILE + c * C::QCHUNK, &tq, q_full, c * C::CH, qp * 256 + t * 128, ga, gb);
+            tma_load_4d(sQ + qs * C::Q_BYTES + t * C::Q_TILE + c * C::QCHUNK, &tq, &q_full[qs], c * C::CH,
+                        qp * 256 + t * 128, ga, gb);
         for (int j = 0; j < nkv; ++j, ++g) {
           const int s = g % NST;
           if (g >= NST) mbar_wait_sleep(&kv_empty[s], ((g / NST) - 1) & 1);
@@ -193,37 +225,38 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     }
     __syncwarp();
   } else if (warp == C::W_MMA || warp == C::W_MMA + 1) {
-    // ===================== MMA issuer (warp 10 idle) =====================
+    // ===================== MMA issuers =====================
+    // SEP: warp W_MMA issues the QK^T MMAs, warp W_MMA + 1 the PV MMAs (an
+    // issuing thread blocks while the tensor pipe is busy, so one role's
+    // issue never delays the other's); otherwise warp W_MMA issues both
     reg_dealloc<C::REG_PRODUCER>();
-    if (warp == C::W_MMA && elect_one()) {
+    if ((warp == C::W_MMA || C::SEP) && elect_one()) {
       constexpr uint32_t idesc_qk = make_idesc(128, SUB, 0, 0, F16);
       constexpr uint32_t idesc_pv = make_idesc(128, C::OW, 0, 1, F16);
       constexpr uint32_t swz = (C::SWB == 128) ? SWZ_128B : SWZ_64B;
       const uint32_t q_addr = smem_u32(sQ);
-      // S(m) = Q_t K_j^T -> buffer m % NB   (j: global KV tile index)
-      auto issue_s = [&](int t, int j, int m) {
+      // S = Q_t K_j^T of item k into TMEM column dS   (j: global KV tile index)
+      auto issue_s = [&](int t, int j, int k, uint32_t dS, uint64_t* bar) {
         const uint32_t ka = smem_u32(sKV + (j % NST) * C::STAGE_BYTES);
-        const uint32_t qa = q_addr + t * C::Q_TILE;
-        const uint32_t dS = tmem + C::COL_S + SUB * (m % NB);
+        const uint32_t qa = q_addr + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE;
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t e = k * 16 / C::CH, w = (k * 16 % C::CH) * 2;
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t e = kk * 16 / C::CH, w = (kk * 16 % C::CH) * 2;
           mma_ss(dS, make_sdesc(qa + e * C::QCHUNK + w, 16, 8 * C::SWB, swz),
-                 make_sdesc(ka + e * C::KCHUNK + w, 16, 8 * C::SWB, swz), idesc_qk, k > 0);
+                 make_sdesc(ka + e * C::KCHUNK + w, 16, 8 * C::SWB, swz), idesc_qk, kk > 0);
         }
-        mma_commit(&s_full[m % NB]);
+        mma_commit(bar);
       };
-      // O_t (+)= P(m) V_j  (+ l_t (+)= P(m) 1)
-      auto issue_pv = [&](int t, int j, int m, bool first, bool last) {
+      // O_t (+)= P V_j  (+ l_t (+)= P 1), P at TMEM column aP
+      auto issue_pv = [&](int t, int j, uint32_t aP, bool first, bool last) {
         const uint32_t va = smem_u32(sKV + (j % NST) * C::STAGE_BYTES + (SHARED ? 0 : C::KV_TILE));
-        const uint32_t aP = tmem + C::COL_S + SUB * (m % NB) + SUB / 2;
         // second MN atom of the B operand: the next V chunk (d = 128) or the ones tile
         const uint32_t vlbo = C::ONES ? smem_u32(sOnes) - va : (uint32_t)C::KCHUNK;
         const uint32_t dO = tmem + (t ? C::COL_O1 : C::COL_O0);
 #pragma unroll
-        for (int k = 0; k < SUB / 16; ++k)
-          mma_ts(dO, aP + 8 * k, make_sdesc(va + k * 16 * C::SWB, vlbo, 8 * C::SWB, swz), idesc_pv,
-                 (!first || k > 0) ? 1u : 0u);
+        for (int kk = 0; kk < SUB / 16; ++kk)
+          mma_ts(dO, aP + 8 * kk, make_sdesc(va + kk * 16 * C::SWB, vlbo, 8 * C::SWB, swz), idesc_pv,
+                 (!first || kk > 0) ? 1u : 0u);
         mma_commit(&o_full[t]);
         if (last) mma_commit(&o_done[t]);
       };
@@ -236,54 +269,118 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         if constexpr (!SHARED) mbar_wait_sleep(&v_full[j % NST], (j / NST) & 1);
         else wait_k(j);
       };
-      const int nS = 2 * nkv;  // score tiles per item
-      int g0 = 0;              // global KV tile index of the item's first tile
-      for (int k = 0; k < my_items; ++k, g0 += nkv) {
-        const int M0 = 2 * g0;  // global score-tile index of the item's first S
-        if constexpr (CONVERT) mbar_wait_sleep(q_conv, k & 1);
-        else mbar_wait_sleep(q_full, k & 1);
-        for (int n = 0; n < NB && n < nS; ++n) {
-          const int t = n & 1, i = n >> 1;
-          if (t == 0) wait_k(g0 + i);
-          tc_fence_after();
-          issue_s(t, g0 + i, M0 + n);
-          if (i == nkv - 1) mma_commit(q_empty);  // Q_t no longer read once this retires
-        }
-        for (int n = 0; n < nS; ++n) {
-          const int t = n & 1, i = n >> 1, m = M0 + n;
-          if (t == 0) wait_v(g0 + i);
-          mbar_wait_sleep(&p_full[m % NB], (m / NB) & 1);
-          TSF_STAMP(p, C::W_MMA, 2 * n);
-          tc_fence_after();
-          if (i == 0 && k > 0) {  // the epilogue of the previous item has read O_t
-            mbar_wait_sleep(&o_empty[t], (k - 1) & 1);
+      auto wait_q = [&](int k) {
+        if constexpr (CONVERT) mbar_wait_sleep(&q_conv[k % C::QST], (k / C::QST) & 1);
+        else mbar_wait_sleep(&q_full[k % C::QST], (k / C::QST) & 1);
+      };
+      if constexpr (C::SEP) {
+        // Per global step G (item G / nkv, KV tile G % nkv), in issue order:
+        //   S_0(G+1) once softmax 0 has loaded S_0(G);  S_1(G+1) likewise;
+        //   PV_0(G) once P_0(G) is stored;  PV_1(G) likewise.
+        // Each tile's next scores are thus computed a full step ahead, and
+        // the tensor pipe (in order) runs PV_t(G) right behind them.
+        const int total = my_items * nkv;
+        if (warp == C::W_MMA) {
+          // QK^T issuer: S_t(G+1) once softmax t has loaded S_t(G)
+          auto issue_next_s = [&](int t, int Gn) {  // S_t(Gn), Gn a global step
+            const int k = Gn / nkv, i = Gn - k * nkv;
+            if (t == 0) {
+              if (i == 0) wait_q(k);
+              wait_k(Gn);
+            }
             tc_fence_after();
+            issue_s(t, Gn, k, tmem + C::COL_S + SUB * t, &s_full[t]);
+            if (i == nkv - 1) mma_commit(&q_empty[k % C::QST]);  // Q_t of item k no longer read by MMAs
+          };
+          if (total > 0) {
+            issue_next_s(0, 0);
+            issue_next_s(1, 0);
           }
-          issue_pv(t, g0 + i, m, i == 0, i == nkv - 1);
-          mma_commit(&kv_empty[(g0 + i) % NST]);  // K_j/V_j free once both tiles' PVs retire
-          const int n2 = n + NB;
-          if (n2 < nS) {
-            const int t2 = n2 & 1, i2 = n2 >> 1;
-            if (t2 == 0) {
-              wait_k(g0 + i2);
+          for (int G = 0; G + 1 < total; ++G) {
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              mbar_wait_sleep(&s_free[t], G & 1);
+              issue_next_s(t, G + 1);
+            }
+          }
+        } else {
+          // PV issuer: PV_t(G) once P_t(G) is stored
+          for (int G = 0; G < total; ++G) {
+            const int k = G / nkv, i = G - k * nkv;
+            wait_v(G);
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              mbar_wait_sleep(&p_full[t], G & 1);
+              TSF_STAMP(p, C::W_MMA, 2 * (2 * i + t));
+              tc_fence_after();
+              if (i == 0 && k > 0) {  // the epilogue of the previous item has read O_t
+                mbar_wait_sleep(&o_empty[t], (k - 1) & 1);
+                tc_fence_after();
+              }
+              issue_pv(t, G, tmem + C::COL_P + (SUB / 2) * t, i == 0, i == nkv - 1);
+              mma_commit(&kv_empty[G % NST]);  // K_j/V_j free once both tiles' PVs retire
+              TSF_STAMP(p, C::W_MMA, 2 * (2 * i + t) + 1);
+            }
+          }
+        }
+      } else {
+        // rotating score buffers: score tile m = 2 g + t in buffer m % NB, its
+        // P in the buffer's upper half; S(m + NB) is issued right after PV(m)
+        const int nS = 2 * nkv;  // score tiles per item
+        int g0 = 0;              // global KV tile index of the item's first tile
+        for (int k = 0; k < my_items; ++k, g0 += nkv) {
+          const int M0 = 2 * g0;  // global score-tile index of the item's first S
+          wait_q(k);
+          for (int n = 0; n < NB && n < nS; ++n) {
+            const int t = n & 1, i = n >> 1, m = M0 + n;
+            if (t == 0) wait_k(g0 + i);
+            tc_fence_after();
+            issue_s(t, g0 + i, k, tmem + C::COL_S + SUB * (m % NB), &s_full[m % NB]);
+            if (i == nkv - 1) mma_commit(&q_empty[k % C::QST]);
+          }
+          for (int n = 0; n < nS; ++n) {
+            const int t = n & 1, i = n >> 1, m = M0 + n;
+            if (t == 0) wait_v(g0 + i);
+            mbar_wait_sleep(&p_full[m % NB], (m / NB) & 1);
+            TSF_STAMP(p, C::W_MMA, 2 * n);
+            tc_fence_after();
+            if (i == 0 && k > 0) {  // the epilogue of the previous item has read O_t
+              mbar_wait_sleep(&o_empty[t], (k - 1) & 1);
               tc_fence_after();
             }
-            issue_s(t2, g0 + i2, M0 + n2);  // reuses buffer m % NB after PV(m) (in order)
-            if (i2 == nkv - 1) mma_commit(q_empty);
+            issue_pv(t, g0 + i, tmem + C::COL_S + SUB * (m % NB) + SUB / 2, i == 0, i == nkv - 1);
+            mma_commit(&kv_empty[(g0 + i) % NST]);
+            const int n2 = n + NB;
+            if (n2 < nS) {
+              const int t2 = n2 & 1, i2 = n2 >> 1, m2 = M0 + n2;
+              if (t2 == 0) {
+                wait_k(g0 + i2);
+                tc_fence_after();
+              }
+              issue_s(t2, g0 + i2, k, tmem + C::COL_S + SUB * (m2 % NB), &s_full[m2 % NB]);
+              if (i2 == nkv - 1) mma_commit(&q_empty[k % C::QST]);
+            }
+            TSF_STAMP(p, C::W_MMA, 2 * n + 1);
           }
-          TSF_STAMP(p, C::W_MMA, 2 * n + 1);
         }
       }
     }
     __syncwarp();
-  } else if (warp < 8) {
+  } else if (warp < C::W_TMA) {
     // ===================== softmax warps =====================
+    // warp w: query tile t = w / (4 SPLIT), column part hf = (w / 4) % SPLIT,
+    // rows (w % 4) * 32 + lane (TMEM lanes are tied to the sub-partition)
     reg_alloc<C::REG_SOFTMAX>();
-    const int t = warp >> 2;                                   // query tile
-    const uint32_t row = (warp & 3) * 32 + lane;               // tile row == TMEM lane
-    const uint32_t lane_base = ((warp & 3) * 32) << 16;
-    const uint32_t tSrow = tmem + lane_base + C::COL_S;
+    constexpr int CW = C::CW;                                  // score columns of this warp
+    constexpr int PW = (CW % 32 == 0) ? 32 : 16;               // exponential pass width
+    const int t = warp / (4 * SPLIT);
+    const int hf = (warp >> 2) % SPLIT;
+    const uint32_t quarter = warp & 3;
+    const uint32_t row = quarter * 32 + lane;                  // tile row == TMEM lane
+    const uint32_t lane_base = (quarter * 32) << 16;
+    const uint32_t tSrow = tmem + lane_base + C::COL_S + hf * CW;
     const uint32_t tOrow = tmem + lane_base + (t ? C::COL_O1 : C::COL_O0);
+    constexpr int OCOLS = D / SPLIT;                           // O columns this warp rescales / stores
     const float sl2 = p.scale_log2;
     const bool pingpong = (p.flags & FLASH_PINGPONG) != 0;
     int G0 = 0;  // global KV tile index of the item's first tile
@@ -294,58 +391,92 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       float l_run = 0.f;        // used when !ONES
 
       for (int i = 0; i < nkv; ++i) {
-        const int G = G0 + i, m = 2 * G + t, b = m % NB;
+        const int G = G0 + i, m = 2 * G + t;
+        // SEP: S_t in its own buffer, P_t in a separate one; else rotating
+        // buffer m % NB with P in its upper half
+        const int b = C::SEP ? t : m % NB;
+        const uint32_t sphase = C::SEP ? (G & 1) : ((m / NB) & 1);
         const uint32_t tSb = tSrow + SUB * b;
+        const uint32_t tPb = C::SEP ? tmem + lane_base + C::COL_P + (SUB / 2) * t + hf * (CW / 2)
+                                    : tSb + SUB / 2;
         TSF_STAMP(p, warp, 6 * i + 0);
-        mbar_wait(&s_full[b], (m / NB) & 1);
+        mbar_wait(&s_full[b], sphase);
         TSF_STAMP(p, warp, 6 * i + 1);
         tc_fence_after();
-        uint32_t sv[SUB];
+        uint32_t sv[CW];
 #pragma unroll
-        for (int c = 0; c < SUB; c += 32) tmem_ld_x32(tSb + c, sv + c);
+        for (int c = 0; c < CW; c += 32) {
+          if (c + 32 <= CW) tmem_ld_x32(tSb + c, sv + c);
+          else tmem_ld_x16(tSb + c, sv + c);
+        }
         tmem_wait_ld();
+        if constexpr (C::SEP) {  // S_t may now be overwritten by S_t(G+1)
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_free[t]);
+        }
         TSF_STAMP(p, warp, 6 * i + 2);
-        const int valid = L - i * SUB;  // columns >= valid are beyond the sequence
-        if (valid < SUB) {
+        const int valid = L - i * SUB - hf * CW;  // columns >= valid are beyond the sequence
+        if (valid < CW) {
 #pragma unroll
-          for (int c = 0; c < SUB; ++c) sv[c] = (c < valid) ? sv[c] : 0xFF800000u;  // -inf
+          for (int c = 0; c < CW; ++c) sv[c] = (c < valid) ? sv[c] : 0xFF800000u;  // -inf
         }
         // row max: 8 independent FMNMX3 chains
         float m8[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) m8[q] = fmaxf(__uint_as_float(sv[2 * q]), __uint_as_float(sv[2 * q + 1]));
 #pragma unroll
-        for (int c = 16; c < SUB; c += 16)
+        for (int c = 16; c < CW; c += 16)
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             m8[q] = max3(m8[q], __uint_as_float(sv[c + 2 * q]), __uint_as_float(sv[c + 2 * q + 1]));
-        const float mx = fmaxf(max3(m8[0], m8[1], m8[2]), max3(m8[3], max3(m8[4], m8[5], m8[6]), m8[7]));
-        if (i == nkv - 1 && EPI != EPI_OUT16) {
+        float mx = fmaxf(max3(m8[0], m8[1], m8[2]), max3(m8[3], max3(m8[4], m8[5], m8[6]), m8[7]));
+        if constexpr (SPLIT > 1) {
+          // the row's other column part: partial maxima through shared memory
+          // (slot by step parity: a partner one step ahead writes the other slot)
+          float* xm = xmax + ((G & 1) * 2 + t) * SPLIT * 128;
+          xm[hf * 128 + row] = mx;
+          named_bar_sync(3 + t * 4 + quarter, 32 * SPLIT);
+#pragma unroll
+          for (int h2 = 0; h2 < SPLIT; ++h2)
+            if (h2 != hf) mx = fmaxf(mx, xm[h2 * 128 + row]);
+        }
+        if (i == nkv - 1 && EPI != EPI_OUT16 && !RES_SMEM) {
           // the epilogue's residual row: start its global read now (L1 prefetch)
           const int l_idx = qp * 256 + t * 128 + (int)row;
           if (l_idx < L) {
             const long long in_off = (long long)l_idx * p.sL + (long long)ga * p.sA + (long long)gb * p.sB;
-            const uint8_t* rp = reinterpret_cast<const uint8_t*>(p.res) + 2 * in_off;
+            const uint8_t* rp = reinterpret_cast<const uint8_t*>(p.res) + 2 * in_off + hf * (2 * OCOLS);
 #pragma unroll
-            for (int c = 0; c < 2 * D; c += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + c));
+            for (int c = 0; c < 2 * OCOLS; c += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + c));
           }
         }
         const float m_new = fmaxf(m_run, mx * sl2);
         TSF_STAMP(p, warp, 6 * i + 3);
+        // Move the max for the whole warp (exact for every row) when some row's
+        // max grew by more than RESCALE_LOG2; O_t (and its l columns) is
+        // rescaled by alpha before P_t is stored, once PV_t(G-1) has retired.
+        // The warps sharing rows see the same maxima, so they decide alike.
+        bool rescale = false;
+        float alpha = 1.f;
         if (i == 0) {
           m_run = m_new;
-        } else {
-          const bool need = (m_new - m_run) > RESCALE_LOG2;
-          if (__any_sync(0xffffffffu, need)) {
-            // Move the max for the whole warp (exact for every row); rescale O_t
-            // (and its l columns) once PV_t(i-1) has retired.
-            const float alpha = ex2(m_run - m_new);
-            l_run *= alpha;
-            m_run = m_new;
+        } else if (__any_sync(0xffffffffu, (m_new - m_run) > RESCALE_LOG2)) {
+          rescale = true;
+          alpha = ex2(m_run - m_new);
+          l_run *= alpha;
+          m_run = m_new;
+        }
+        auto before_p_store = [&]() {
+          // SEP: P_t's buffer is free once PV_t(G-1) retired (every step); the
+          // rescale needs the same (O_t final for this step)
+          if ((C::SEP && G > 0) || rescale) {
             mbar_wait(&o_full[t], (G - 1) & 1);
             tc_fence_after();
+          }
+          if (rescale) {
 #pragma unroll
-            for (int c = 0; c < D; c += 32) {
+            for (int c = hf * OCOLS; c < (hf + 1) * OCOLS; c += 32) {
               uint32_t ov[32];
               tmem_ld_x32(tOrow + c, ov);
               tmem_wait_ld();
@@ -353,7 +484,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
               for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
               tmem_st_x32(tOrow + c, ov);
             }
-            if (C::ONES) {
+            if (C::ONES && hf == SPLIT - 1) {
               uint32_t lv[8];
               tmem_ld_x8(tOrow + D, lv);
               tmem_wait_ld();
@@ -362,24 +493,28 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
               tmem_st_x8(tOrow + D, lv);
             }
           }
-        }
-        // ping-pong: the two warpgroups take turns for the exponential phase
+        };
+        // ping-pong: the two tiles' warps take turns for the exponential phase
         // (MUFU-bound), so one's exps overlap the other's waits / max / stores
-        if (pingpong && !(t == 0 && G == 0)) named_bar_sync(1 + t, 256);
+        if (pingpong && !(t == 0 && G == 0)) named_bar_sync(1 + t, 256 * SPLIT);
         const float nmb = -m_run;
         float ls0 = 0.f, ls1 = 0.f;
+        // SEP: all of P_t is packed in registers and stored after the last
+        // exponential, so the wait for PV_t(G-1) (P_t's buffer) is at the end
+        uint32_t pk_all[C::SEP ? CW / 2 : 1];
 #pragma unroll
-        for (int c0 = 0; c0 < SUB; c0 += 32) {
-          // three passes over 32 columns (scale, exponentiate, pack) so no
+        for (int c0 = 0; c0 < CW; c0 += PW) {
+          // three passes over PW columns (scale, exponentiate, pack) so no
           // MUFU result is consumed right after it is issued (in-order issue)
-          float xv[32], pv[32];
-          uint32_t pk[16];
+          float xv[PW], pv[PW];
+          uint32_t pk_local[C::SEP ? 1 : PW / 2];
+          uint32_t* pk = C::SEP ? pk_all + c0 / 2 : pk_local;
 #pragma unroll
-          for (int c = 0; c < 32; c += 2)
+          for (int c = 0; c < PW; c += 2)
             ffma2(xv[c], xv[c + 1], __uint_as_float(sv[c0 + c]), __uint_as_float(sv[c0 + c + 1]), sl2, sl2, nmb,
                   nmb);
 #pragma unroll
-          for (int c = 0; c < 32; c += 2) {
+          for (int c = 0; c < PW; c += 2) {
             if (((c >> 1) & 7) >= 8 - EMU / 2) {
               ex2_poly2(pv[c], pv[c + 1], xv[c], xv[c + 1]);   // FMA/ALU pipes
             } else {
@@ -388,28 +523,40 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
             }
           }
 #pragma unroll
-          for (int c = 0; c < 32; c += 2) {
+          for (int c = 0; c < PW; c += 2) {
             pk[c / 2] = pack2<F16>(pv[c], pv[c + 1]);
             if constexpr (!C::ONES) { ls0 += pv[c]; ls1 += pv[c + 1]; }
           }
-          tmem_st_x16(tSb + SUB / 2 + c0 / 2, pk);
+          if constexpr (!C::SEP) {
+            if (c0 == 0) before_p_store();
+            if constexpr (PW == 32) tmem_st_x16(tPb + c0 / 2, pk);
+            else tmem_st_x8(tPb + c0 / 2, pk);
+          }
         }
-        if (pingpong) named_bar_arrive(2 - t, 256);
+        if constexpr (C::SEP) {
+          before_p_store();
+#pragma unroll
+          for (int c0 = 0; c0 < CW; c0 += PW) {
+            if constexpr (PW == 32) tmem_st_x16(tPb + c0 / 2, pk_all + c0 / 2);
+            else tmem_st_x8(tPb + c0 / 2, pk_all + c0 / 2);
+          }
+        }
+        if (pingpong) named_bar_arrive(2 - t, 256 * SPLIT);
         l_run += ls0 + ls1;
         TSF_STAMP(p, warp, 6 * i + 4);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[b]);
+        if (lane == 0) mbar_arrive(&p_full[C::SEP ? t : b]);
         TSF_STAMP(p, warp, 6 * i + 5);
       }
 
-      // ---- epilogue of item k ----
+      // ---- epilogue of item k: this warp's OCOLS columns of its rows ----
       mbar_wait(&o_done[t], k & 1);
       tc_fence_after();
-      float o[D];
+      float o[OCOLS];
 #pragma unroll
-      for (int c = 0; c < D; c += 32) tmem_ld_x32(tOrow + c, reinterpret_cast<uint32_t*>(o + c));
+      for (int c = 0; c < OCOLS; c += 32) tmem_ld_x32(tOrow + hf * OCOLS + c, reinterpret_cast<uint32_t*>(o + c));
       if constexpr (C::ONES) {
         uint32_t lv[8];
         tmem_ld_x8(tOrow + D, lv);
@@ -424,6 +571,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       const int l_idx = qp * 256 + t * 128 + (int)row;
       if (l_idx < L) {
         const long long in_off = (long long)l_idx * p.sL + (long long)ga * p.sA + (long long)gb * p.sB;
+        constexpr int NU = OCOLS / 8;
         if (EPI == EPI_BLOCK_T && p.P > 1) {
           // distributed temporal stage: frame l_idx belongs to rank l_idx / Kc
           const int dst = l_idx / p.Kc;
@@ -431,14 +579,22 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           q.o = p.peer_out[dst];
           const long long off = (long long)(l_idx - dst * p.Kc) * p.osL + (long long)ga * p.osA +
                                 (long long)(gb + p.b_off) * p.osB;
-          epilogue_row_g<D, EPI, D / 8>(q, o, 1.0f / l_run, off, in_off, 0);
+          epilogue_row_g<D, EPI, NU>(q, o, 1.0f / l_run, off, in_off, hf * NU);
+        } else if (RES_SMEM_OK && RES_SMEM) {
+          const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
+          epilogue_row<D, 128, EPI, NU>(p, o, 1.0f / l_run, off,
+                                        sQ + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE, row, hf * NU);
         } else {
           const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
-          epilogue_row_g<D, EPI, D / 8>(p, o, 1.0f / l_run, off, in_off, 0);
+          epilogue_row_g<D, EPI, NU>(p, o, 1.0f / l_run, off, in_off, hf * NU);
         }
       }
+      if (RES_SMEM) {  // this warp's rows of Q_t (item k) read: the next Q may load
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&q_empty[k % C::QST]);
+      }
     }  // items
-    if (pingpong && t == 0 && my_items > 0) named_bar_sync(1, 256);  // consume tile 1's last turn
+    if (pingpong && t == 0 && my_items > 0) named_bar_sync(1, 256 * SPLIT);  // consume tile 1's last turn
   } else {
     // ===================== converter warp (block temporal stage) =====================
     reg_dealloc<C::REG_PRODUCER>();
@@ -481,10 +637,11 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       static_assert((SUB * 2 * D / 16 / 32) % 8 == 0, "conversion batching");
       int g = 0;
       for (int k = 0; k < my_items; ++k) {
-        mbar_wait(q_full, k & 1);
-        convert_tile(sQ, 128);
-        convert_tile(sQ + C::Q_TILE, 128);
-        if (lane == 0) mbar_arrive(q_conv);
+        const int qs = k % C::QST;
+        mbar_wait(&q_full[qs], (k / C::QST) & 1);
+        convert_tile(sQ + qs * C::Q_BYTES, 128);
+        convert_tile(sQ + qs * C::Q_BYTES + C::Q_TILE, 128);
+        if (lane == 0) mbar_arrive(&q_conv[qs]);
         for (int j = 0; j < nkv; ++j, ++g) {
           const int s = g % NST;
           mbar_wait(&k_full[s], (g / NST) & 1);

@@ -222,6 +222,17 @@ static int flash_sub(int d) {
   return 96;
 }
 
+// Softmax warps per score row in the d = 64 flash kernel (1 | 2): TSF_SPLIT
+// overrides the default for experiments.
+static int flash_split() {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("TSF_SPLIT");
+    env = e ? atoi(e) : -1;
+  }
+  return env == 2 ? 2 : 1;  // 2: measured slower at C2 (the row-max exchange serialises the pair)
+}
+
 template <int D, int EPI, int EMU, int SUB>
 static tsf_status launch_flash_sub(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
                                    const CUtensorMap& mv, const AttnParams& p) {
@@ -239,8 +250,15 @@ static tsf_status launch_flash_sub(tsf_handle* h, cudaStream_t st, const CUtenso
   pp.flags = flags_env;
   // persistent: one CTA per SM, each loops over work items
   const long long grid = items < h->num_sms ? items : h->num_sms;
-  using C = FlashCfg<D, EPI, NST, SUB>;
-  return launch(h, attn_flash_kernel<D, EPI, NST, EMU, SUB>, (int)grid, C::THREADS, C::SMEM, st, pp, mq, mk, mv);
+  if constexpr (FlashCfg<D, EPI, NST, SUB>::SEP && FlashCfg<D, EPI, NST, SUB>::ONES) {
+    if (flash_split() == 2) {
+      using C = FlashCfg<D, EPI, NST, SUB, 2>;
+      return launch(h, attn_flash_kernel<D, EPI, NST, EMU, SUB, 2>, (int)grid, C::THREADS, C::SMEM, st, pp, mq, mk,
+                    mv);
+    }
+  }
+  using C = FlashCfg<D, EPI, NST, SUB, 1>;
+  return launch(h, attn_flash_kernel<D, EPI, NST, EMU, SUB, 1>, (int)grid, C::THREADS, C::SMEM, st, pp, mq, mk, mv);
 }
 
 template <int D, int EPI, int EMU>

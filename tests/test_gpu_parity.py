@@ -52,6 +52,8 @@ ATTN_SHAPES = [
     (33, 1, 3, 32),      # N=1: spatial = v exactly
     (128, 40, 2, 64),    # temporal packed with L=128 (G=1)
     (2, 100, 4, 32),     # spatial packed N=100 (WIN=128)
+    (8, 1000, 40, 64),   # spatial flash with ~4 work items per persistent CTA (Q/S/P buffer reuse)
+    (300, 8, 64, 32),    # temporal flash d=32 with several work items per CTA
 ]
 
 
@@ -94,7 +96,9 @@ def test_degenerate_reductions_exact(tsf_lib):
 
 
 BLOCK_SHAPES = [(4, 64, 2, 32), (8, 300, 2, 64), (12, 130, 3, 64), (5, 256, 2, 128), (200, 4, 2, 64),
-                (1, 129, 2, 64), (9, 1, 2, 32)]
+                (1, 129, 2, 64), (9, 1, 2, 32),
+                (8, 1000, 40, 64),   # spatial stage: ~4 work items per persistent CTA (Q slots, residual from smem)
+                (260, 6, 40, 64)]    # temporal flash stage (converter warp): several items per CTA
 
 
 @pytest.mark.parametrize("shape", BLOCK_SHAPES)

@@ -32,32 +32,34 @@ def main():
         run()
     torch.cuda.synchronize()
     L = tsf.lib()
-    buf = (ctypes.c_ulonglong * (16 * PER_WARP))()
+    buf = (ctypes.c_ulonglong * (32 * PER_WARP))()
     L.tsf_trace_read.restype = ctypes.c_int
-    L.tsf_trace_read(layer._h, buf, 16 * PER_WARP)        # clear
+    L.tsf_trace_read(layer._h, buf, 32 * PER_WARP)        # clear
     run()
     torch.cuda.synchronize()
-    L.tsf_trace_read(layer._h, buf, 16 * PER_WARP)
-    a = np.frombuffer(buf, dtype=np.uint64).reshape(16, PER_WARP).astype(np.int64)
+    L.tsf_trace_read(layer._h, buf, 32 * PER_WARP)
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(32, PER_WARP).astype(np.int64)
     sub = int(os.environ.get("TSF_SUB", "96" if d == 64 else "128"))
     nsub = (N + sub - 1) // sub
     t0 = a[a > 0].min()
     print(f"{what} TSF_EMU={os.environ.get('TSF_EMU', 'default')} nsub={nsub}  kernel span (CTA0 stamps) {a.max() - t0} cycles")
     phases = ["wait S", "ld S", "max", "exp+st", "arrive", "to next"]
-    for w in range(8):
+    split = int(os.environ.get("TSF_SPLIT", "2" if d == 64 else "1"))
+    wmma = 8 * split + 1
+    for w in range(8 * split):
         s = a[w, :6 * nsub].reshape(nsub, 6)
         dif = np.diff(s, axis=1)
         nxt = s[1:, 0] - s[:-1, 5]
         per = dif.mean(0).tolist() + [nxt.mean()]
         tot = (s[-1, 5] - s[0, 0]) / nsub
         print(f"warp {w}: cycles/sub-step {tot:7.1f} | " + " ".join(f"{p} {v:6.1f}" for p, v in zip(phases, per)))
-    m = a[9, :4 * nsub].reshape(2 * nsub, 2)
-    print(f"MMA warp 9: mean cycles p_full->issued {np.diff(m, axis=1).mean():.1f}, "
+    m = a[wmma, :4 * nsub].reshape(2 * nsub, 2)
+    print(f"MMA warp {wmma}: mean cycles p_full->issued {np.diff(m, axis=1).mean():.1f}, "
           f"issued->next p_full {(m[1:, 0] - m[:-1, 1]).mean():.1f}")
     print("first sub-steps, warp 0 and warp 4 (relative to kernel start):")
     for i in range(min(6, nsub)):
-        print(i, (a[0, 6 * i:6 * i + 6] - t0).tolist(), (a[4, 6 * i:6 * i + 6] - t0).tolist(),
-              (a[9, 4 * i:4 * i + 4] - t0).tolist())
+        print(i, (a[0, 6 * i:6 * i + 6] - t0).tolist(), (a[4 * split, 6 * i:6 * i + 6] - t0).tolist(),
+              (a[wmma, 4 * i:4 * i + 4] - t0).tolist())
     os.makedirs("gpurun_out", exist_ok=True)
     np.save("gpurun_out/trace_flash.npy", a)
 

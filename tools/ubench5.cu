@@ -7,12 +7,13 @@ constexpr int NMMA = 2048;
 
 template <int N, bool TS>
 __global__ void bench(long long* cyc) {
-  __shared__ __align__(1024) uint8_t sa[128 * 128];
-  __shared__ __align__(1024) uint8_t sb[128 * 128];
+  __shared__ __align__(1024) uint8_t sab[256 * 128];  // B up to N = 256 rows; A aliases it
+  uint8_t* sa = sab;
+  uint8_t* sb = sab;
   __shared__ uint64_t bar;
   __shared__ uint32_t holder;
   for (int i = threadIdx.x; i < 128 * 128 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sa)[i] = 0x3c003c00u;
-  for (int i = threadIdx.x; i < 128 * 128 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sb)[i] = 0x3c003c00u;
+  for (int i = threadIdx.x; i < 256 * 128 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sb)[i] = 0x3c003c00u;
   fence_proxy_async_smem();
   if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
   if (threadIdx.x < 32) tmem_alloc<512>(&holder);
@@ -54,7 +55,8 @@ void run(long long* cyc) {
 int main() {
   long long* cyc;
   cudaMallocManaged(&cyc, 64);
-  run<16, false>(cyc); run<32, false>(cyc); run<64, false>(cyc); run<128, false>(cyc);
-  run<16, true>(cyc); run<64, true>(cyc); run<128, true>(cyc);
+  run<16, false>(cyc); run<32, false>(cyc); run<64, false>(cyc); run<96, false>(cyc); run<128, false>(cyc);
+  run<192, false>(cyc); run<256, false>(cyc);
+  run<16, true>(cyc); run<64, true>(cyc); run<80, true>(cyc); run<96, true>(cyc); run<128, true>(cyc); run<144, true>(cyc); run<256, true>(cyc);
   return 0;
 }
