@@ -80,6 +80,7 @@ struct AttnParams {
   int flags;
 };
 constexpr int FLASH_PINGPONG = 2;
+constexpr int FLASH_RES_GLOBAL = 4;  // flash kernel: block residual from global memory, not the Q tile (diagnostics)
 
 constexpr int MAX_PEERS = 8;
 // per-destination output tensor maps (packed kernel, distributed temporal stage)

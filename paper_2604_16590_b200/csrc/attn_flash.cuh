@@ -109,8 +109,10 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
   constexpr bool SHARED = C::SHARED;
   // block spatial stage: the residual X_t row is the query row itself (q = X_t),
   // so the epilogue reads it from the Q tile in shared memory (Q double-buffered)
-  constexpr bool RES_SMEM_OK = C::SEP && EPI == EPI_BLOCK_S;
-  const bool RES_SMEM = RES_SMEM_OK && !(p.flags & 4);
+  // (block temporal stage: the Q tile holds fp16(x), converted in place; equal
+  // to the bf16 x except below 2^-14 in magnitude, where it differs by < 2^-25)
+  constexpr bool RES_SMEM_OK = C::SEP && EPI != EPI_OUT16;
+  const bool RES_SMEM = RES_SMEM_OK && !(p.flags & FLASH_RES_GLOBAL);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                        // QST x (Q0 | Q1)
@@ -579,7 +581,11 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           q.o = p.peer_out[dst];
           const long long off = (long long)(l_idx - dst * p.Kc) * p.osL + (long long)ga * p.osA +
                                 (long long)(gb + p.b_off) * p.osB;
-          epilogue_row_g<D, EPI, NU>(q, o, 1.0f / l_run, off, in_off, hf * NU);
+          if (RES_SMEM_OK && RES_SMEM)
+            epilogue_row<D, 128, EPI, NU>(q, o, 1.0f / l_run, off,
+                                          sQ + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE, row, hf * NU);
+          else
+            epilogue_row_g<D, EPI, NU>(q, o, 1.0f / l_run, off, in_off, hf * NU);
         } else if (RES_SMEM_OK && RES_SMEM) {
           const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
           epilogue_row<D, 128, EPI, NU>(p, o, 1.0f / l_run, off,
