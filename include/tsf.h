@@ -86,7 +86,10 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
 
 /* Same as tsf_spacetime_block with HOST buffers (pinned memory recommended):
  * copies x host->device, runs the block, copies y device->host and
- * synchronises `stream`.  Staging buffers are allocated on first use. */
+ * synchronises `stream`.  Staging buffers (and, single GPU, a copy stream)
+ * are allocated on first use.  Single GPU: the spatial stage runs in up to 4
+ * frame chunks and each chunk's y is copied out while the next one computes;
+ * the result is bitwise the device call's. */
 tsf_status tsf_spacetime_block_host(tsf_handle* h, const tsf_bf16* x_host, float* y_host, void* stream);
 
 /* Release the workspace (and the NCCL communicator of a distributed handle;

@@ -62,7 +62,12 @@ struct tsf_handle {
   int* d_flag = nullptr;        // 1-int NCCL all-reduce = cross-rank barrier
   PeerMaps pm{};                // per-destination output maps of the current launch
   bool use_pm = false;
+  // host API (single GPU): the spatial stage runs in frame chunks and each
+  // chunk's y copy to the host overlaps the next chunk's compute
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> ev_h;         // [HOST_CHUNKS + 1]
 };
+constexpr int HOST_CHUNKS = 4;
 
 // Output routing of the distributed temporal stage (run_attention).
 struct DistOut {
@@ -627,6 +632,8 @@ void tsf_destroy(tsf_handle* h) {
   for (auto e : h->ev_t) cudaEventDestroy(e);
   for (auto e : h->ev_a) cudaEventDestroy(e);
   if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+  for (auto e : h->ev_h) cudaEventDestroy(e);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   for (auto e : h->event_pool) cudaEventDestroy(e);
   free_workspace(h);
   if (h->trace) cudaFree(h->trace);
@@ -881,6 +888,47 @@ tsf_status tsf_spacetime_block_host(tsf_handle* h, const tsf_bf16* x_host, float
     StageTimer tm(h, st, 3);
     TSF_CUDA(h, cudaMemcpyAsync(h->xdev, x_host, in_bytes, cudaMemcpyHostToDevice, st));
     tm.done();
+  }
+  if (P == 1 && h->K >= 2) {
+    // temporal stage whole (it needs every frame of a token), then the spatial
+    // stage in frame chunks: chunk c's y goes to the host on copy_stream while
+    // chunk c+1 computes (y is frame-major, so a chunk is contiguous)
+    if (!h->copy_stream) {
+      TSF_CUDA(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+      h->ev_h.resize(HOST_CHUNKS + 1);
+      for (auto& e : h->ev_h) TSF_CUDA(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    h->launches = 0;
+    const __nv_bfloat16* xd = h->xdev;
+    tsf_status s;
+    {
+      StageTimer tm(h, st, 0);
+      s = run_attention(h, temporal_view(h->K, h->N, h->H, h->d), xd, xd, xd, EPI_BLOCK_T, h->xt, nullptr, st);
+      tm.done();
+      if (s != TSF_OK) return s;
+    }
+    const int nch = h->K < HOST_CHUNKS ? h->K : HOST_CHUNKS;
+    const size_t frame = (size_t)h->N * h->H * h->d;
+    int f0 = 0;
+    for (int c = 0; c < nch; ++c) {
+      const int f1 = (int)(((long long)h->K * (c + 1)) / nch);
+      {
+        StageTimer tm(h, st, 1);
+        s = run_attention(h, spatial_view(f1 - f0, h->N, h->H, h->d), h->xt + f0 * frame, h->xt + f0 * frame,
+                          h->xt + f0 * frame, EPI_BLOCK_S, nullptr, h->ydev + f0 * frame, st);
+        tm.done();
+        if (s != TSF_OK) return s;
+      }
+      TSF_CUDA(h, cudaEventRecord(h->ev_h[c], st));
+      TSF_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_h[c], 0));
+      TSF_CUDA(h, cudaMemcpyAsync(y_host + f0 * frame, h->ydev + f0 * frame, (f1 - f0) * frame * sizeof(float),
+                                  cudaMemcpyDeviceToHost, h->copy_stream));
+      f0 = f1;
+    }
+    TSF_CUDA(h, cudaEventRecord(h->ev_h[HOST_CHUNKS], h->copy_stream));
+    TSF_CUDA(h, cudaStreamWaitEvent(st, h->ev_h[HOST_CHUNKS], 0));  // the next call's stage buffers
+    TSF_CUDA(h, cudaStreamSynchronize(st));
+    return TSF_OK;
   }
   tsf_status s = tsf_spacetime_block(h, reinterpret_cast<const tsf_bf16*>(h->xdev), h->ydev, stream);
   if (s != TSF_OK) return s;

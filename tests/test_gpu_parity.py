@@ -162,8 +162,10 @@ def test_full_size_attention_sampled(tsf_lib, cfg):
           f"{cfg} spatial sampled")
 
 
-def test_block_host_api_matches_device_api(tsf_lib):
-    K, N, H, d = 8, 300, 2, 64
+@pytest.mark.parametrize("shape", [(8, 300, 2, 64), (5, 260, 3, 64), (1, 200, 2, 32), (3, 64, 2, 128)])
+def test_block_host_api_matches_device_api(tsf_lib, shape):
+    """Host-buffer API (spatial stage in frame chunks, y copied out per chunk) == device API, bitwise."""
+    K, N, H, d = shape
     xb = synth.make_x(K, N, H, d, seed=8)
     layer = tsf_lib.Layer(K, N, H, d)
     y_dev = layer.block(to_dev(xb))
