@@ -73,13 +73,19 @@ struct FlashCfg {
   // softmax warps per SM sub-partition to keep MUFU busy.  Needs SEP and the
   // ones-column denominator (no partial row sums to combine).
   static constexpr int SPLIT = SPLIT_;
+  static constexpr int NSOFT_ = 8 * SPLIT_;
   static_assert(SPLIT == 1 || (SPLIT == 2 && SEP && ONES), "SPLIT = 2 needs SEP and d = 64");
   static constexpr int CW = SUB / SPLIT;                   // score columns per softmax warp
   static_assert(CW % 16 == 0, "columns per warp");
   static constexpr int QST = SEP ? 2 : 1;                  // Q stages (double-buffered when SMEM allows)
   static constexpr int XMAX_BYTES = SPLIT > 1 ? 2 * 2 * SPLIT * 128 * 4 : 0;  // [parity][tile][half][row]
   static constexpr int BAR_BYTES = 1024;
-  static constexpr int SMEM = QST * Q_BYTES + NST * STAGE_BYTES + ONES_BYTES + XMAX_BYTES + BAR_BYTES + 1024;
+  // distributed block temporal stage: each softmax warp stages its 32 X_t rows
+  // in shared memory so the stores to peer ranks go out as whole 2d-byte rows
+  // (UPR lanes per row) instead of one 16-byte piece per thread and row
+  static constexpr int EPI_STAGE = (SEP && SPLIT == 1 && EPI == EPI_BLOCK_T) ? NSOFT_ * 32 * 2 * D : 0;
+  static constexpr int SMEM =
+      QST * Q_BYTES + NST * STAGE_BYTES + ONES_BYTES + XMAX_BYTES + EPI_STAGE + BAR_BYTES + 1024;
   static_assert(SMEM <= 227 * 1024, "shared memory");
   static_assert(SUB % 32 == 0 && SUB >= 64 && SUB <= 128, "KV tile rows");
   static constexpr uint32_t COL_O0 = 0, COL_O1 = OW, COL_S = 2 * OW;
@@ -119,7 +125,8 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
   uint8_t* sKV = smem + C::QST * C::Q_BYTES; // NST x (K | V)
   uint8_t* sOnes = sKV + NST * C::STAGE_BYTES;
   float* xmax = reinterpret_cast<float*>(sOnes + C::ONES_BYTES);  // SPLIT > 1: [2][2][SPLIT][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES + C::XMAX_BYTES);
+  uint8_t* sEpi = sOnes + C::ONES_BYTES + C::XMAX_BYTES;  // EPI_STAGE: [softmax warp][32 rows][2 d bytes]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + C::EPI_STAGE);
   uint64_t* q_full = bars;                   // [QST]
   uint64_t* k_full = bars + C::QST;          // [NST]
   uint64_t* v_full = k_full + NST;           // [NST]
@@ -571,7 +578,38 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[t]);  // the next item's PV may overwrite O_t
       const int l_idx = qp * 256 + t * 128 + (int)row;
-      if (l_idx < L) {
+      bool staged = false;
+      if constexpr (C::EPI_STAGE > 0) {
+        if (p.P > 1 && RES_SMEM) {
+          // distributed temporal stage: X_t rows staged per warp, then written
+          // to their owner ranks (frame l belongs to rank l / Kc) UPR lanes per row
+          staged = true;
+          uint8_t* stw = sEpi + warp * (32 * 2 * D);
+          const bool ok = l_idx < L;
+          int dst = 0;
+          long long off = 0;
+          if (ok) {
+            dst = l_idx / p.Kc;
+            off = (long long)(l_idx - dst * p.Kc) * p.osL + (long long)ga * p.osA + (long long)(gb + p.b_off) * p.osB;
+            epilogue_row_stage<D, 128, 32>(o, 1.0f / l_run, sQ + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE, row, stw,
+                                           lane);
+          }
+          __syncwarp();
+          constexpr int UPR = 2 * D / 16;  // 16-byte units per row
+          constexpr int RPI = 32 / UPR;    // rows per warp store
+#pragma unroll
+          for (int j = 0; j < 32 / RPI; ++j) {
+            const int r = j * RPI + (int)lane / UPR, u = (int)lane % UPR;
+            const int rd = __shfl_sync(0xffffffffu, dst, r);
+            const long long ro = __shfl_sync(0xffffffffu, off, r);
+            const int rok = __shfl_sync(0xffffffffu, (int)ok, r);
+            if (rok)
+              *reinterpret_cast<uint4*>(static_cast<__half*>(p.peer_out[rd]) + ro + 8 * u) = tile_row_u4<D, 32>(stw, r, u);
+          }
+          __syncwarp();  // the staging tile is rewritten at the next item
+        }
+      }
+      if (l_idx < L && !staged) {
         const long long in_off = (long long)l_idx * p.sL + (long long)ga * p.sA + (long long)gb * p.sB;
         constexpr int NU = OCOLS / 8;
         if (EPI == EPI_BLOCK_T && p.P > 1) {
