@@ -1012,8 +1012,17 @@ tsf_status tsf_transpose(tsf_handle* h, int A, int B, const tsf_bf16* in, tsf_bf
   cudaStream_t st = (cudaStream_t)stream;
   const int vecs = h->H * h->d * 2 / 16;
   StageTimer tm(h, st, 4);
-  transpose_rows_kernel<<<grid_for(h, (long long)A * B * vecs), 256, 0, st>>>((const uint4*)in, (uint4*)out, nullptr,
-                                                                               nullptr, A, B, vecs);
+  static int variant = -1;
+  if (variant < 0) {
+    const char* e = getenv("TSF_TRANSPOSE");
+    variant = e ? atoi(e) : 1;
+  }
+  if (variant == 1)
+    transpose_rows_ilp_kernel<<<grid_for(h, ((long long)A * B * vecs + 3) / 4), 256, 0, st>>>(
+        (const uint4*)in, (uint4*)out, A, B, vecs);
+  else
+    transpose_rows_kernel<<<grid_for(h, (long long)A * B * vecs), 256, 0, st>>>((const uint4*)in, (uint4*)out,
+                                                                                 nullptr, nullptr, A, B, vecs);
   TSF_CUDA(h, cudaGetLastError());
   tm.done();
   h->launches++;
