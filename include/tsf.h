@@ -46,7 +46,7 @@ typedef struct tsf_handle tsf_handle; /* opaque */
 typedef enum {
   TSF_OK = 0,
   TSF_ERR_CONFIG = 2,      /* bad size, null/misaligned/aliased pointer, K%P or N%P != 0 */
-  TSF_ERR_NUMERIC = 3,     /* reserved: non-finite input (debug builds only) */
+  TSF_ERR_NUMERIC = 3,     /* non-finite block intermediate X_t (fp16 overflow or non-finite x), see tsf_sync */
   TSF_ERR_UNSUPPORTED = 4, /* d not in {32, 64, 128}, or device is not sm_100 */
   TSF_ERR_CUDA = 5,        /* CUDA runtime/driver failure (launch, copy, tensor map) */
   TSF_ERR_NCCL = 6,        /* NCCL failure */
@@ -78,7 +78,11 @@ tsf_status tsf_spatial_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k,
  *   X_t = x + T(x, x, x);   y = X_t + S(X_t, X_t, X_t).
  * x: bf16.  y: fp32.  X_t is kept in fp16 (11-bit mantissa, reading G8): the
  * spatial stage's MMAs read it (with fp16 P) and the residual adds it.
- * Precondition: |X_t| < 65504 (fp16 range), e.g. |x| < 32752.
+ * Range: |X_t| must stay below 65504 (fp16), e.g. |x| < 32752.  The temporal
+ * epilogue checks every stored X_t element; a non-finite one (overflow, or a
+ * non-finite x) sets the handle's flag, reported as TSF_ERR_NUMERIC by the next
+ * tsf_sync (and by tsf_spacetime_block_host, which synchronises).  y is then
+ * not meaningful.
  * Single GPU: x, y are [K, N, H, d].  Distributed: x is the token shard
  * [K, N/P, H, d], y the frame shard [K/P, N, H, d]; one all-to-all (NCCL,
  * bytes, bit-exact) reshards X_t between the stages. */
@@ -91,6 +95,17 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
  * frame chunks and each chunk's y is copied out while the next one computes;
  * the result is bitwise the device call's. */
 tsf_status tsf_spacetime_block_host(tsf_handle* h, const tsf_bf16* x_host, float* y_host, void* stream);
+
+/* Wait for `stream` and report what the asynchronous work found:
+ *   TSF_ERR_NUMERIC  a block since the last tsf_sync stored a non-finite X_t
+ *                    (the flag is cleared);
+ *   TSF_ERR_NCCL     (distributed handles) NCCL reported an asynchronous error
+ *                    while waiting, or timeout_ms > 0 elapsed first: then the
+ *                    communicator is aborted (a dead or hung peer cannot hang
+ *                    this rank forever) and later collective calls on h fail;
+ *   TSF_ERR_CUDA     the stream reported a CUDA error.
+ * timeout_ms <= 0 waits without a limit.  Polls the stream (no blocking sync). */
+tsf_status tsf_sync(tsf_handle* h, void* stream, int timeout_ms);
 
 /* Release the workspace (and the NCCL communicator of a distributed handle;
  * aborted instead of destroyed if it reports an asynchronous error). */
@@ -107,6 +122,22 @@ tsf_status tsf_get_unique_id(void* id128);
  * device.  Requires K % world == 0 and N % world == 0. */
 tsf_status tsf_create_dist(int K, int N, int H, int d, const void* id128, int rank, int world,
                            tsf_handle** out);
+
+/* One-GPU simulation of P ranks (validation of the distributed path without P
+ * GPUs; BASELINE.json north_star: "the all-to-all reshard must be bit-exact").
+ * The handle runs every virtual rank's share of the distributed block on the
+ * current device with the same code as tsf_create_dist handles: the same
+ * kernels, output routing and per-destination tensor maps, the same byte plan
+ * and unpack kernel.  Only the transport differs: the ranks' buffers are local
+ * and device copies stand in for NCCL send/recv.  exchange_mode: 1 = NCCL byte
+ * plan (send/recv + unpack), 2 = fused scatter (the temporal kernel stores X_t
+ * rows into every rank's frame shard).  2 <= P <= 8, K % P == N % P == 0.
+ * On such a handle the calls take ALL virtual ranks' shards back to back:
+ *   tsf_spacetime_block: x = [P][K][N/P][H][d] (rank r's token shard at
+ *     r*K*(N/P)*H*d), y = [P][K/P][N][H][d] (= the full frame-major [K,N,H,d]);
+ *   tsf_reshard: the same stacking of token and frame shards.
+ * tsf_temporal_attn / tsf_spatial_attn act on one shard (rank 0's shapes). */
+tsf_status tsf_create_sim(int K, int N, int H, int d, int P, int exchange_mode, tsf_handle** out);
 
 /* Reshard a bf16 tensor between the two shardings (pure data movement,
  * bit-exact): TSF_T2S: in = token shard [K, N/P, H, d] -> out = frame shard
@@ -135,6 +166,9 @@ int tsf_last_launch_count(const tsf_handle* h);
  * IPC mappings; a 1-int NCCL all-reduce orders the stores).  Shapes the fused
  * scatter cannot tile use mode 1 per call.  Returns -1 for NULL. */
 int tsf_exchange_mode(const tsf_handle* h);
+
+/* Number of ranks of h (1 single GPU; P distributed or simulated); -1 for NULL. */
+int tsf_world_size(const tsf_handle* h);
 
 /* Stage timing with CUDA events recorded on the call's stream around each
  * stage's kernel(s).  tsf_set_timing(h, 1) starts recording (clearing earlier

@@ -42,6 +42,9 @@ SIGNATURES = [
     ("tsf_destroy", None, [_P]),
     ("tsf_get_unique_id", _I, [_P]),
     ("tsf_create_dist", _I, [_I, _I, _I, _I, _P, _I, _I, ctypes.POINTER(_P)]),
+    ("tsf_create_sim", _I, [_I, _I, _I, _I, _I, _I, ctypes.POINTER(_P)]),
+    ("tsf_sync", _I, [_P, _P, _I]),
+    ("tsf_world_size", _I, [_P]),
     ("tsf_reshard", _I, [_P, _I, _P, _P, _P]),
     ("tsf_transpose", _I, [_P, _I, _I, _P, _P, _P]),
     ("tsf_last_error", ctypes.c_char_p, [_P]),
@@ -107,11 +110,17 @@ class Layer:
     process per GPU); None = single GPU.
     """
 
-    def __init__(self, K: int, N: int, H: int, d: int, group=None):
+    def __init__(self, K: int, N: int, H: int, d: int, group=None, sim_world: int = 0, sim_mode: int = 2):
         self.K, self.N, self.H, self.d = K, N, H, d
         self._h = ctypes.c_void_p()
+        self.sim = sim_world > 0
         L = lib()
-        if group is None:
+        if self.sim:
+            # one-GPU simulation of sim_world ranks (tsf_create_sim): the calls take
+            # every virtual rank's shard stacked on a leading axis
+            self.world, self.rank = sim_world, 0
+            _check(L.tsf_create_sim(K, N, H, d, sim_world, sim_mode, ctypes.byref(self._h)))
+        elif group is None:
             self.world, self.rank = 1, 0
             _check(L.tsf_create(K, N, H, d, ctypes.byref(self._h)))
         else:
@@ -129,14 +138,16 @@ class Layer:
             uid = (ctypes.c_char * 128).from_buffer_copy(raw)
             _check(L.tsf_create_dist(K, N, H, d, uid, self.rank, self.world, ctypes.byref(self._h)))
 
-    # shapes of the shards this rank holds
+    # shapes of the shards this rank holds (a simulated handle: all ranks' shards stacked)
     @property
     def token_shard_shape(self):
-        return (self.K, self.N // self.world, self.H, self.d)
+        s = (self.K, self.N // self.world, self.H, self.d)
+        return (self.world,) + s if self.sim else s
 
     @property
     def frame_shard_shape(self):
-        return (self.K // self.world, self.N, self.H, self.d)
+        s = (self.K // self.world, self.N, self.H, self.d)
+        return (self.world,) + s if self.sim else s
 
     def close(self):
         if self._h:
@@ -159,7 +170,7 @@ class Layer:
     def temporal(self, q, k, v, out=None, stream=None):
         """tsf_temporal_attn: q, k, v bf16 [K, N/P, H, d] -> bf16 (P:64 temporal)."""
         import torch
-        shp = self.token_shard_shape
+        shp = self.token_shard_shape[-4:]
         for t, n in ((q, "q"), (k, "k"), (v, "v")):
             _need(t, torch.bfloat16, shp, n)
         out = torch.empty_like(q) if out is None else out
@@ -171,7 +182,7 @@ class Layer:
     def spatial(self, q, k, v, out=None, stream=None):
         """tsf_spatial_attn: q, k, v bf16 [K/P, N, H, d] -> bf16 (P:64 spatial)."""
         import torch
-        shp = self.frame_shard_shape
+        shp = self.frame_shard_shape[-4:]
         for t, n in ((q, "q"), (k, "k"), (v, "v")):
             _need(t, torch.bfloat16, shp, n)
         out = torch.empty_like(q) if out is None else out
@@ -220,6 +231,11 @@ class Layer:
         _need(out, torch.bfloat16, (B, A, self.H, self.d), "out")
         _check(lib().tsf_transpose(self._h, A, B, x.data_ptr(), out.data_ptr(), _stream_ptr(stream)), self._h)
         return out
+
+    def sync(self, stream=None, timeout_ms: int = 0):
+        """tsf_sync: wait for the stream; raises TsfError(TSF_ERR_NUMERIC) if a block stored a
+        non-finite X_t, TsfError(TSF_ERR_NCCL) on an NCCL error or timeout (communicator aborted)."""
+        _check(lib().tsf_sync(self._h, _stream_ptr(stream), int(timeout_ms)), self._h)
 
     # ---- accounting ----
     def last_launch_count(self) -> int:

@@ -78,6 +78,10 @@ struct AttnParams {
   // flash kernel schedule: FLASH_PINGPONG (the two softmax warpgroups take
   // turns for the exponential phase)
   int flags;
+  // block temporal stage: set to 1 (plain store, host-mapped memory) when a
+  // stored fp16 X_t element is +-inf or NaN (|x + T(x)| beyond the fp16 range,
+  // or a non-finite input); reported as TSF_ERR_NUMERIC by tsf_sync
+  unsigned int* nonfinite;
 };
 constexpr int FLASH_PINGPONG = 2;
 constexpr int FLASH_RES_GLOBAL = 4;  // flash kernel: block residual from global memory, not the Q tile (diagnostics)
@@ -121,6 +125,22 @@ __device__ __forceinline__ float2 unpack2(uint32_t w) {
   }
 }
 
+// Non-finite detector for a pair of fp16 values: an fp16 is +-inf or NaN iff
+// its exponent field is all ones (0x7C00); adding 0x0400 to the masked
+// exponent then carries into bit 15 of that half (and only then; no carry
+// crosses into the upper half).  OR-accumulate and test once per row.
+__device__ __forceinline__ uint32_t f16x2_nonfinite_bits(uint32_t w) {
+  return ((w & 0x7C007C00u) + 0x04000400u) & 0x80008000u;
+}
+__device__ __forceinline__ uint32_t u4_nonfinite_bits(const uint4& w) {
+  return f16x2_nonfinite_bits(w.x) | f16x2_nonfinite_bits(w.y) | f16x2_nonfinite_bits(w.z) |
+         f16x2_nonfinite_bits(w.w);
+}
+// Report a row's accumulated non-finite bits (rare path: one plain store).
+__device__ __forceinline__ void report_nonfinite(const AttnParams& p, uint32_t nf) {
+  if (__builtin_expect(nf != 0u, 0) && p.nonfinite) *reinterpret_cast<volatile unsigned int*>(p.nonfinite) = 1u;
+}
+
 // Byte offset of 16-byte unit u of row r in a TMA/UMMA swizzled tile whose
 // rows are SWB bytes (128 -> SWIZZLE_128B, 64 -> SWIZZLE_64B).
 template <int SWB>
@@ -144,9 +164,10 @@ __device__ __forceinline__ uint4 tile_row_u4(const uint8_t* tile, uint32_t r, ui
 // memory (the swizzled Q tile).
 // NU 16-byte units starting at unit u0 (o_acc holds those 8 * NU values).
 template <int D, int ROWS, int EPI, int NU = D / 8>
-__device__ __forceinline__ void epilogue_row(const AttnParams& p, const float* o_acc, float inv_l,
+__device__ __forceinline__ uint32_t epilogue_row(const AttnParams& p, const float* o_acc, float inv_l,
                                              long long off, const uint8_t* res_tile, uint32_t r, int u0 = 0) {
   constexpr bool F16 = EpiTraits<EPI>::F16;
+  uint32_t nf = 0;
   off += 8 * u0;
 #pragma unroll
   for (int u = 0; u < NU; ++u) {
@@ -176,18 +197,21 @@ __device__ __forceinline__ void epilogue_row(const AttnParams& p, const float* o
         w.y = pack2<true>(x1.x + v[2], x1.y + v[3]);
         w.z = pack2<true>(x2.x + v[4], x2.y + v[5]);
         w.w = pack2<true>(x3.x + v[6], x3.y + v[7]);
+        nf |= u4_nonfinite_bits(w);
         *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.o) + off + 8 * u) = w;
       }
     }
   }
+  return nf;
 }
 
 // Flash-kernel epilogue for NU units starting at unit u0 of one row, residual
 // read from global memory at element offset in_off (EPI_BLOCK_T: bf16 x,
 // EPI_BLOCK_S: fp16 X_t); output at element offset off of p.o / p.y.
 template <int D, int EPI, int NU>
-__device__ __forceinline__ void epilogue_row_g(const AttnParams& p, const float* o_acc, float inv_l, long long off,
+__device__ __forceinline__ uint32_t epilogue_row_g(const AttnParams& p, const float* o_acc, float inv_l, long long off,
                                                long long in_off, int u0) {
+  uint32_t nf = 0;
   off += 8 * u0;
   in_off += 8 * u0;
 #pragma unroll
@@ -219,19 +243,22 @@ __device__ __forceinline__ void epilogue_row_g(const AttnParams& p, const float*
         w.y = pack2<true>(x1.x + v[2], x1.y + v[3]);
         w.z = pack2<true>(x2.x + v[4], x2.y + v[5]);
         w.w = pack2<true>(x3.x + v[6], x3.y + v[7]);
+        nf |= u4_nonfinite_bits(w);
         *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.o) + off + 8 * u) = w;
       }
     }
   }
+  return nf;
 }
 
 // Epilogue for one row written back IN PLACE into its swizzled shared-memory
 // row (the tile the row's input came from), for a TMA store of the whole tile.
 // EPI_OUT16: bf16(O/l); EPI_BLOCK_T: fp16(x + O/l) with x read from the same row.
 template <int D, int ROWS, int EPI>
-__device__ __forceinline__ void epilogue_row_smem(const float* o_acc, float inv_l, uint8_t* tile, uint32_t r) {
+__device__ __forceinline__ uint32_t epilogue_row_smem(const float* o_acc, float inv_l, uint8_t* tile, uint32_t r) {
   constexpr int SWB = (2 * D < 128) ? 2 * D : 128;
   constexpr int UPC = SWB / 16;
+  uint32_t nf = 0;
 #pragma unroll
   for (int u = 0; u < D / 8; ++u) {
     uint4* ptr = reinterpret_cast<uint4*>(tile + (u / UPC) * (ROWS * SWB) + swz_off<SWB>(r, u % UPC));
@@ -252,18 +279,21 @@ __device__ __forceinline__ void epilogue_row_smem(const float* o_acc, float inv_
       w.y = pack2<true>(x1.x + v[2], x1.y + v[3]);
       w.z = pack2<true>(x2.x + v[4], x2.y + v[5]);
       w.w = pack2<true>(x3.x + v[6], x3.y + v[7]);
+      nf |= u4_nonfinite_bits(w);
     }
     *ptr = w;
   }
+  return nf;
 }
 
 // EPI_BLOCK_T epilogue into a separate staging tile: x from res_tile row r,
 // X_t = fp16(x + O/l) written to row orow of out_tile (same swizzled layout).
 template <int D, int ROWS_IN, int ROWS_OUT>
-__device__ __forceinline__ void epilogue_row_stage(const float* o_acc, float inv_l, const uint8_t* res_tile,
+__device__ __forceinline__ uint32_t epilogue_row_stage(const float* o_acc, float inv_l, const uint8_t* res_tile,
                                                    uint32_t r, uint8_t* out_tile, uint32_t orow) {
   constexpr int SWB = (2 * D < 128) ? 2 * D : 128;
   constexpr int UPC = SWB / 16;
+  uint32_t nf = 0;
 #pragma unroll
   for (int u = 0; u < D / 8; ++u) {
     const uint4 rr = tile_row_u4<D, ROWS_IN>(res_tile, r, u);
@@ -277,8 +307,10 @@ __device__ __forceinline__ void epilogue_row_stage(const float* o_acc, float inv
     w.y = pack2<true>(x1.x + v[2], x1.y + v[3]);
     w.z = pack2<true>(x2.x + v[4], x2.y + v[5]);
     w.w = pack2<true>(x3.x + v[6], x3.y + v[7]);
+    nf |= u4_nonfinite_bits(w);
     *reinterpret_cast<uint4*>(out_tile + (u / UPC) * (ROWS_OUT * SWB) + swz_off<SWB>(orow, u % UPC)) = w;
   }
+  return nf;
 }
 
 }  // namespace tsf

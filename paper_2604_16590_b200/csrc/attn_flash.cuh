@@ -591,8 +591,8 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           if (ok) {
             dst = l_idx / p.Kc;
             off = (long long)(l_idx - dst * p.Kc) * p.osL + (long long)ga * p.osA + (long long)(gb + p.b_off) * p.osB;
-            epilogue_row_stage<D, 128, 32>(o, 1.0f / l_run, sQ + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE, row, stw,
-                                           lane);
+            report_nonfinite(p, epilogue_row_stage<D, 128, 32>(o, 1.0f / l_run, sQ + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE, row, stw,
+                                           lane));
           }
           __syncwarp();
           constexpr int UPR = 2 * D / 16;  // 16-byte units per row
@@ -620,17 +620,17 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           const long long off = (long long)(l_idx - dst * p.Kc) * p.osL + (long long)ga * p.osA +
                                 (long long)(gb + p.b_off) * p.osB;
           if (RES_SMEM_OK && RES_SMEM)
-            epilogue_row<D, 128, EPI, NU>(q, o, 1.0f / l_run, off,
-                                          sQ + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE, row, hf * NU);
+            report_nonfinite(p, epilogue_row<D, 128, EPI, NU>(q, o, 1.0f / l_run, off,
+                                          sQ + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE, row, hf * NU));
           else
-            epilogue_row_g<D, EPI, NU>(q, o, 1.0f / l_run, off, in_off, hf * NU);
+            report_nonfinite(p, epilogue_row_g<D, EPI, NU>(q, o, 1.0f / l_run, off, in_off, hf * NU));
         } else if (RES_SMEM_OK && RES_SMEM) {
           const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
-          epilogue_row<D, 128, EPI, NU>(p, o, 1.0f / l_run, off,
-                                        sQ + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE, row, hf * NU);
+          report_nonfinite(p, epilogue_row<D, 128, EPI, NU>(p, o, 1.0f / l_run, off,
+                                        sQ + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE, row, hf * NU));
         } else {
           const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
-          epilogue_row_g<D, EPI, NU>(p, o, 1.0f / l_run, off, in_off, hf * NU);
+          report_nonfinite(p, epilogue_row_g<D, EPI, NU>(p, o, 1.0f / l_run, off, in_off, hf * NU));
         }
       }
       if (RES_SMEM) {  // this warp's rows of Q_t (item k) read: the next Q may load

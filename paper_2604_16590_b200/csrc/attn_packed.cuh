@@ -262,7 +262,7 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
         named_bar_sync(1, 128);
         if (row_ok) {
           const int dst = li / Kc, orow = dst * rows_per_dst + (li - dst * Kc) + Kc * gi;
-          epilogue_row_stage<D, 128, 128>(o, 1.0f / l, smem + s * C::STAGE_BYTES, r, stage_out, orow);
+          report_nonfinite(p, epilogue_row_stage<D, 128, 128>(o, 1.0f / l, smem + s * C::STAGE_BYTES, r, stage_out, orow));
         }
         fence_proxy_async_smem();
         named_bar_sync(1, 128);
@@ -277,7 +277,7 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
         }
       } else if constexpr (TMA_OUT) {
         // rows into the stage's (first) tile in place, then one TMA store
-        if (row_ok) epilogue_row_smem<D, 128, EPI>(o, 1.0f / l, smem + s * C::STAGE_BYTES, r);
+        if (row_ok) report_nonfinite(p, epilogue_row_smem<D, 128, EPI>(o, 1.0f / l, smem + s * C::STAGE_BYTES, r));
         fence_proxy_async_smem();
         named_bar_sync(1, 128);
         if (threadIdx.x == 0) {
@@ -300,7 +300,7 @@ attn_packed_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
         const int a = a0 + gi % p.Ab, b = b0 + gi / p.Ab;
         if (row_ok && b < p.B && l > 0.f) {
           const long long off = (long long)li * p.osL + (long long)a * p.osA + (long long)b * p.osB;
-          epilogue_row<D, 128, EPI>(p, o, 1.0f / l, off, smem + s * C::STAGE_BYTES, r);
+          report_nonfinite(p, epilogue_row<D, 128, EPI>(p, o, 1.0f / l, off, smem + s * C::STAGE_BYTES, r));
         }
         named_bar_sync(1, 128);
         if (threadIdx.x == 0) mbar_arrive(&empty[s]);

@@ -8,11 +8,13 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "attn_flash.cuh"
@@ -66,6 +68,17 @@ struct tsf_handle {
   // chunk's y copy to the host overlaps the next chunk's compute
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> ev_h;         // [HOST_CHUNKS + 1]
+  // small device scratch allocated before the (collective) communicator init:
+  // [0] 1-int all-reduce barrier, [16] agreement flag, [256..] IPC handle all-gather
+  char* scratch = nullptr;
+  bool comm_dead = false;                // aborted by tsf_sync's timeout
+  // non-finite X_t flag (host-mapped, written by the temporal epilogue)
+  volatile unsigned int* nf_host = nullptr;
+  unsigned int* nf_dev = nullptr;
+  // one-GPU simulation of `world` ranks (tsf_create_sim): xt / rxt / uxt hold
+  // every virtual rank's buffer back to back; sim_mode 1 = NCCL byte plan with
+  // device copies in place of send/recv, 2 = fused scatter
+  bool sim = false;
 };
 constexpr int HOST_CHUNKS = 4;
 
@@ -77,6 +90,7 @@ struct DistOut {
 
 static thread_local std::string g_create_err;
 extern "C" void tsf_destroy(tsf_handle* h);
+extern "C" tsf_status tsf_sync(tsf_handle* h, void* stream, int timeout_ms);
 
 // ---------------------------------------------------------------------------
 // helpers
@@ -364,6 +378,7 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
   p.o = o;
   p.y = y;
   p.res = q;  // the block's residual input (q = k = v there)
+  p.nonfinite = h->nf_dev;
 #ifdef TSF_TRACE
   if (!h->trace) {
     cudaMalloc(&h->trace, 32 * TRACE_PER_WARP * sizeof(unsigned long long));
@@ -471,12 +486,25 @@ static tsf_status check_shape(int K, int N, int H, int d, int world) {
 }
 
 static tsf_status alloc_workspace(tsf_handle* h) {
-  const size_t El = (size_t)h->K * (h->N / h->world) * h->H * h->d;  // token-shard elements
+  // token-shard elements (times the virtual ranks of a simulated handle)
+  const size_t El = (size_t)h->K * (h->N / h->world) * h->H * h->d * (h->sim ? h->world : 1);
   auto a = [&](__half** p, size_t n) -> bool {
     return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(__half)) == cudaSuccess;
   };
   bool ok = a(&h->xt, El);
   if (ok && h->world > 1) ok = a(&h->rxt, El) && a(&h->uxt, El);
+  if (ok && h->world > 1 && !h->sim)
+    ok = cudaMalloc(reinterpret_cast<void**>(&h->scratch), 256 + (size_t)h->world * 2 * sizeof(cudaIpcMemHandle_t)) ==
+         cudaSuccess;
+  if (ok) {
+    unsigned int* hp = nullptr;
+    ok = cudaHostAlloc(reinterpret_cast<void**>(&hp), sizeof(unsigned int), cudaHostAllocMapped) == cudaSuccess;
+    if (ok) {
+      *hp = 0u;
+      h->nf_host = hp;
+      ok = cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->nf_dev), hp, 0) == cudaSuccess;
+    }
+  }
   if (!ok) {
     cudaGetLastError();
     return fail(nullptr, TSF_ERR_NOMEM, "workspace cudaMalloc failed");
@@ -485,8 +513,14 @@ static tsf_status alloc_workspace(tsf_handle* h) {
 }
 
 static void free_workspace(tsf_handle* h) {
-  for (void* p : {(void*)h->xt, (void*)h->rxt, (void*)h->uxt, (void*)h->xdev, (void*)h->ydev})
+  for (void* p : {(void*)h->xt, (void*)h->rxt, (void*)h->uxt, (void*)h->xdev, (void*)h->ydev, (void*)h->scratch})
     if (p) cudaFree(p);
+  if (h->nf_host) cudaFreeHost(const_cast<unsigned int*>(h->nf_host));
+  h->xt = h->rxt = h->uxt = nullptr;
+  h->xdev = nullptr;
+  h->ydev = nullptr;
+  h->scratch = nullptr;
+  h->nf_host = nullptr;
 }
 
 // ---------------------------------------------------------------------------
@@ -529,6 +563,9 @@ tsf_status tsf_create_dist(int K, int N, int H, int d, const void* id128, int ra
   tsf_handle* h = new tsf_handle();
   h->K = K; h->N = N; h->H = H; h->d = d;
   h->rank = rank; h->world = world;
+  // everything the setup below needs on the device (workspace, the barrier
+  // int, the agreement flag, the IPC-handle exchange buffer) is allocated
+  // BEFORE the collective communicator init
   if ((s = check_device(nullptr, &h->device, &h->num_sms)) != TSF_OK || (s = alloc_workspace(h)) != TSF_OK) {
     free_workspace(h);
     delete h;
@@ -539,8 +576,8 @@ tsf_status tsf_create_dist(int K, int N, int H, int d, const void* id128, int ra
     memcpy(&id, id128, sizeof id);
     ncclResult_t r = ncclCommInitRank(&h->comm, world, id, rank);
     if (r != ncclSuccess) {
-      free_workspace(h);
-      delete h;
+      h->comm = nullptr;
+      tsf_destroy(h);
       return fail(nullptr, TSF_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     }
     // head chunks of the NCCL fallback path (exchange / spatial overlap):
@@ -563,53 +600,87 @@ tsf_status tsf_create_dist(int K, int N, int H, int d, const void* id128, int ra
       cudaEventCreateWithFlags(&h->ev_t[c], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&h->ev_a[c], cudaEventDisableTiming);
     }
-    // fused exchange: all-gather the IPC handles of every rank's two frame-shard
-    // X_t buffers and map them
+    h->d_flag = reinterpret_cast<int*>(h->scratch);
+    int* d_ok = reinterpret_cast<int*>(h->scratch + 16);
+    char* dh = h->scratch + 256;
+    cudaStream_t cs = h->comm_stream;
+    // every rank takes part in every collective below, whatever its local
+    // outcome, so the sequence of collectives is identical on all ranks
+    auto agree = [&](bool local_ok) -> bool {  // all-reduce (min) of the local outcome
+      int v = local_ok ? 1 : 0;
+      if (cudaMemcpy(d_ok, &v, sizeof v, cudaMemcpyHostToDevice) != cudaSuccess) v = 0;
+      if (ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, h->comm, cs) != ncclSuccess ||
+          cudaStreamSynchronize(cs) != cudaSuccess || cudaMemcpy(&v, d_ok, sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return false;
+      return v == 1;
+    };
+    // fused exchange: all-gather the IPC handles of every rank's two
+    // frame-shard X_t buffers and map them (TSF_FUSED_EXCHANGE=0 disables it
+    // on every rank: the environment is the job's)
     const char* fe = getenv("TSF_FUSED_EXCHANGE");
-    if (world <= MAX_PEERS && !(fe && atoi(fe) == 0)) {
+    const bool want = world <= MAX_PEERS && !(fe && atoi(fe) == 0);
+    if (want) {
       const size_t El = (size_t)h->K * (h->N / world) * h->H * h->d;
       h->ubuf[0] = h->uxt;
       cudaIpcMemHandle_t mine[2];
-      char* dh = nullptr;
+      memset(mine, 0, sizeof mine);
       bool ok = cudaMalloc(reinterpret_cast<void**>(&h->ubuf[1]), El * sizeof(__half)) == cudaSuccess &&
                 cudaIpcGetMemHandle(&mine[0], h->ubuf[0]) == cudaSuccess &&
-                cudaIpcGetMemHandle(&mine[1], h->ubuf[1]) == cudaSuccess &&
-                cudaMalloc(&dh, (size_t)world * sizeof mine) == cudaSuccess &&
-                cudaMalloc(&h->d_flag, sizeof(int)) == cudaSuccess &&
-                cudaMemcpy(dh + rank * sizeof mine, mine, sizeof mine, cudaMemcpyHostToDevice) == cudaSuccess;
-      std::vector<cudaIpcMemHandle_t> all(2 * world);
-      if (ok) ok = ncclAllGather(dh + rank * sizeof mine, dh, sizeof mine, ncclUint8, h->comm, h->comm_stream) ==
-                   ncclSuccess &&
-                   cudaStreamSynchronize(h->comm_stream) == cudaSuccess &&
+                cudaIpcGetMemHandle(&mine[1], h->ubuf[1]) == cudaSuccess;
+      cudaGetLastError();
+      ok = cudaMemcpy(dh + rank * sizeof mine, mine, sizeof mine, cudaMemcpyHostToDevice) == cudaSuccess && ok;
+      bool fused = agree(ok);
+      if (fused) {
+        std::vector<cudaIpcMemHandle_t> all(2 * world);
+        bool ok2 = ncclAllGather(dh + rank * sizeof mine, dh, sizeof mine, ncclUint8, h->comm, cs) == ncclSuccess &&
+                   cudaStreamSynchronize(cs) == cudaSuccess &&
                    cudaMemcpy(all.data(), dh, (size_t)world * sizeof mine, cudaMemcpyDeviceToHost) == cudaSuccess;
-      for (int p = 0; ok && p < world; ++p)
-        for (int b = 0; ok && b < 2; ++b) {
-          if (p == rank) h->peer_buf[b][p] = h->ubuf[b];
-          else ok = cudaIpcOpenMemHandle(&h->peer_buf[b][p], all[2 * p + b], cudaIpcMemLazyEnablePeerAccess) ==
-                    cudaSuccess;
-        }
+        for (int p = 0; ok2 && p < world; ++p)
+          for (int b = 0; ok2 && b < 2; ++b) {
+            if (p == rank) h->peer_buf[b][p] = h->ubuf[b];
+            else ok2 = cudaIpcOpenMemHandle(&h->peer_buf[b][p], all[2 * p + b], cudaIpcMemLazyEnablePeerAccess) ==
+                       cudaSuccess;
+          }
+        cudaGetLastError();
+        fused = agree(ok2);
+      }
+      if (!fused) {  // close whatever was opened; fall back to the NCCL path
+        for (int b = 0; b < 2; ++b)
+          for (int p = 0; p < world && p < MAX_PEERS; ++p) {
+            if (h->peer_buf[b][p] && p != rank) cudaIpcCloseMemHandle(h->peer_buf[b][p]);
+            h->peer_buf[b][p] = nullptr;
+          }
+      }
       int fc = 1;
       if (const char* e = getenv("TSF_FUSED_CHUNKS")) fc = atoi(e);
       if (fc < 1 || h->H % fc) fc = 1;
       h->fchunks = fc;
       h->ev_f.resize(fc + 1);
       for (auto& e : h->ev_f) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-      if (dh) cudaFree(dh);
-      cudaGetLastError();
-      // every rank must agree on the mode: all-reduce (min) of the local outcome
-      int* d_ok = nullptr;
-      int v = ok ? 1 : 0;
-      if (cudaMalloc(&d_ok, sizeof(int)) == cudaSuccess &&
-          cudaMemcpy(d_ok, &v, sizeof v, cudaMemcpyHostToDevice) == cudaSuccess &&
-          ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, h->comm, h->comm_stream) == ncclSuccess &&
-          cudaStreamSynchronize(h->comm_stream) == cudaSuccess)
-        cudaMemcpy(&v, d_ok, sizeof v, cudaMemcpyDeviceToHost);
-      else
-        v = 0;
-      if (d_ok) cudaFree(d_ok);
-      h->fused = v == 1;
+      h->fused = fused;
     }
   }
+  *out = h;
+  return TSF_OK;
+}
+
+tsf_status tsf_create_sim(int K, int N, int H, int d, int P, int exchange_mode, tsf_handle** out) {
+  if (!out) return fail(nullptr, TSF_ERR_CONFIG, "out is null");
+  *out = nullptr;
+  if (P < 2 || P > MAX_PEERS) return fail(nullptr, TSF_ERR_CONFIG, "simulated world size must be in [2, 8]");
+  if (exchange_mode != 1 && exchange_mode != 2) return fail(nullptr, TSF_ERR_CONFIG, "exchange_mode must be 1 or 2");
+  tsf_status s = check_shape(K, N, H, d, P);
+  if (s != TSF_OK) return s;
+  tsf_handle* h = new tsf_handle();
+  h->K = K; h->N = N; h->H = H; h->d = d;
+  h->world = P;
+  h->sim = true;
+  if ((s = check_device(nullptr, &h->device, &h->num_sms)) != TSF_OK || (s = alloc_workspace(h)) != TSF_OK) {
+    free_workspace(h);
+    delete h;
+    return s;
+  }
+  h->fused = exchange_mode == 2;
   *out = h;
   return TSF_OK;
 }
@@ -628,7 +699,6 @@ void tsf_destroy(tsf_handle* h) {
       if (h->peer_buf[b][p] && p != h->rank) cudaIpcCloseMemHandle(h->peer_buf[b][p]);
   if (h->ubuf[1]) cudaFree(h->ubuf[1]);
   for (auto e : h->ev_f) cudaEventDestroy(e);
-  if (h->d_flag) cudaFree(h->d_flag);
   for (auto e : h->ev_t) cudaEventDestroy(e);
   for (auto e : h->ev_a) cudaEventDestroy(e);
   if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
@@ -649,6 +719,8 @@ int tsf_exchange_mode(const tsf_handle* h) {
   if (h->world <= 1) return 0;
   return h->fused ? 2 : 1;
 }
+
+int tsf_world_size(const tsf_handle* h) { return h ? h->world : -1; }
 
 tsf_status tsf_set_timing(tsf_handle* h, int enable) {
   if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
@@ -705,16 +777,55 @@ tsf_status tsf_spatial_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k,
   return s;
 }
 
-// X_t token shard -> frame shard for head chunk c: one grouped NCCL send/recv
-// round (bytes, bit-exact) on the comm stream.  Chunk c of X_t is
-// [K][N/P][Hc][d]; its frames [p K/P, (p+1) K/P) (contiguous) go to peer p;
-// the receive buffer is [P][K/P][N/P][Hc][d].
-static tsf_status exchange_chunk(tsf_handle* h, int c, cudaStream_t cs) {
-  const int P = h->world, Kc = h->K / P, Nc = h->N / P, Hc = h->H / h->nchunk;
-  const size_t chunk_elems = (size_t)h->K * Nc * Hc * h->d;
-  const size_t peer_bytes = (size_t)Kc * Nc * Hc * h->d * 2;
-  const char* src = reinterpret_cast<const char*>(h->xt + c * chunk_elems);
-  char* dst = reinterpret_cast<char*>(h->rxt + c * chunk_elems);
+// ---------------------------------------------------------------------------
+// Distributed block pieces.  The multi-process path (one rank per GPU) and the
+// one-GPU simulation of P ranks (tsf_create_sim) run the SAME pieces: the same
+// run_attention calls (output routing, per-destination tensor maps, kernels),
+// the same byte plan and unpack kernel.  Only the transport differs: NCCL
+// send/recv and CUDA IPC peer pointers vs device copies and local buffers.
+// ---------------------------------------------------------------------------
+
+// Temporal stage of rank `rank` with the fused exchange: X_t rows go straight
+// into every rank's frame shard (peers[r]); vin is the rank's token-shard view
+// (all heads, or one head chunk).
+static tsf_status temporal_fused(tsf_handle* h, const View& vin, const tsf_bf16* x, int rank, void* const* peers,
+                                 cudaStream_t st) {
+  const DistOut dist{h->world, h->K / h->world, rank, h->N / h->world, peers};
+  StageTimer tm(h, st, 0);
+  tsf_status s = run_attention(h, vin, x, x, x, EPI_BLOCK_T, nullptr, nullptr, st, nullptr, &dist);
+  tm.done();
+  return s;
+}
+
+// NCCL-path temporal stage of head chunk c: X_t token shard chunk
+// [K][N/P][Hc][d] into xt (rank-local).
+static tsf_status temporal_tokens(tsf_handle* h, const tsf_bf16* x, __half* xt, int c, cudaStream_t st) {
+  const int nc = h->nchunk, Hc = h->H / nc, K = h->K, Nl = h->N / h->world, H = h->H, d = h->d;
+  const size_t chunk_elems = (size_t)K * Nl * Hc * d;
+  const View vin{K, Hc, Nl, (long long)Nl * H * d, (long long)d, (long long)H * d};
+  const View vout{K, Hc, Nl, (long long)Nl * Hc * d, (long long)d, (long long)Hc * d};
+  const tsf_bf16* xc = x + (size_t)c * Hc * d;
+  StageTimer tm(h, st, 0);
+  tsf_status s = run_attention(h, vin, xc, xc, xc, EPI_BLOCK_T, xt + c * chunk_elems, nullptr, st, &vout);
+  tm.done();
+  return s;
+}
+
+// Byte plan of the exchange of head chunk c: chunk c of X_t is
+// [K][N/P][Hc][d]; its frames [p K/P, (p+1) K/P) (contiguous, peer_bytes)
+// go to peer p, which stores them at slot `rank` of its receive buffer
+// [P][K/P][N/P][Hc][d].  Untyped bytes: bit-exact.
+static size_t exchange_peer_bytes(const tsf_handle* h) {
+  return (size_t)(h->K / h->world) * (h->N / h->world) * (h->H / h->nchunk) * h->d * 2;
+}
+static size_t chunk_elems(const tsf_handle* h) {
+  return (size_t)h->K * (h->N / h->world) * (h->H / h->nchunk) * h->d;
+}
+static tsf_status exchange_chunk(tsf_handle* h, int c, cudaStream_t cs) {  // NCCL transport
+  const int P = h->world;
+  const size_t peer_bytes = exchange_peer_bytes(h);
+  const char* src = reinterpret_cast<const char*>(h->xt + c * chunk_elems(h));
+  char* dst = reinterpret_cast<char*>(h->rxt + c * chunk_elems(h));
   TSF_NCCL(h, ncclGroupStart());
   for (int p = 0; p < P; ++p) {
     TSF_NCCL(h, ncclSend(src + p * peer_bytes, peer_bytes, ncclUint8, p, h->comm, cs));
@@ -723,18 +834,89 @@ static tsf_status exchange_chunk(tsf_handle* h, int c, cudaStream_t cs) {
   TSF_NCCL(h, ncclGroupEnd());
   return TSF_OK;
 }
+// The same byte plan with device copies between the simulated ranks'
+// buffers (base[r] = rank r's buffer, El elements apart).
+static tsf_status exchange_sim(tsf_handle* h, const __half* src_base, __half* dst_base, size_t stride_elems,
+                               size_t src_off, size_t dst_off, size_t peer_bytes, cudaStream_t st) {
+  const int P = h->world;
+  for (int r = 0; r < P; ++r)
+    for (int p = 0; p < P; ++p) {
+      const char* src = reinterpret_cast<const char*>(src_base + r * stride_elems + src_off) + p * peer_bytes;
+      char* dst = reinterpret_cast<char*>(dst_base + p * stride_elems + dst_off) + r * peer_bytes;
+      TSF_CUDA(h, cudaMemcpyAsync(dst, src, peer_bytes, cudaMemcpyDeviceToDevice, st));
+    }
+  return TSF_OK;
+}
 
 // receive buffer [P][K/P][N/P][Hc][d] of chunk c -> frame shard [K/P][N][Hc][d]
-static tsf_status unpack_chunk(tsf_handle* h, int c, cudaStream_t st) {
+static tsf_status unpack_chunk(tsf_handle* h, const __half* rxt, __half* uxt, int c, cudaStream_t st) {
   const int P = h->world, Kc = h->K / P, Nc = h->N / P, Hc = h->H / h->nchunk;
-  const size_t chunk_elems = (size_t)h->K * Nc * Hc * h->d;
   const int vecs = Hc * h->d * 2 / 16;
   const long long items = (long long)P * Kc * Nc * vecs;
-  reshard_perm_kernel<true><<<grid_for(h, items), 256, 0, st>>>((const uint4*)(h->rxt + c * chunk_elems),
-                                                                (uint4*)(h->uxt + c * chunk_elems), nullptr,
+  reshard_perm_kernel<true><<<grid_for(h, items), 256, 0, st>>>((const uint4*)(rxt + c * chunk_elems(h)),
+                                                                (uint4*)(uxt + c * chunk_elems(h)), nullptr,
                                                                 nullptr, P, Kc, Nc, vecs);
   TSF_CUDA(h, cudaGetLastError());
   h->launches++;
+  return TSF_OK;
+}
+
+// Spatial stage of a frame shard: u = X_t [K/P][N][H][d] (chunk layout
+// [c][K/P][N][Hc][d] when `chunked`), y fp32 [K/P][N][H][d].
+static tsf_status spatial_shard(tsf_handle* h, const __half* u, float* y, int nc, int c, bool chunked,
+                                cudaStream_t st) {
+  const int Kl = h->K / h->world, N = h->N, H = h->H, d = h->d, Hc = H / nc;
+  const View vy{N, Hc, Kl, (long long)H * d, (long long)d, (long long)N * H * d};
+  const View vs = chunked ? View{N, Hc, Kl, (long long)Hc * d, (long long)d, (long long)N * Hc * d} : vy;
+  const __half* uc = u + (chunked ? c * chunk_elems(h) : (size_t)c * Hc * d);
+  StageTimer tm(h, st, 1);
+  tsf_status s = run_attention(h, vs, uc, uc, uc, EPI_BLOCK_S, nullptr, y + (size_t)c * Hc * d, st, &vy);
+  tm.done();
+  return s;
+}
+
+static tsf_status check_comm(tsf_handle* h) {
+  if (h->world <= 1 || h->sim) return TSF_OK;
+  if (h->comm_dead || !h->comm) return fail(h, TSF_ERR_NCCL, "communicator aborted (tsf_sync timeout or error)");
+  ncclResult_t ae = ncclSuccess;
+  if (ncclCommGetAsyncError(h->comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress)
+    return fail(h, TSF_ERR_NCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(ae));
+  return TSF_OK;
+}
+
+// One-GPU simulation of the distributed block: x = the P token shards back
+// to back ([P][K][N/P][H][d]), y = the P frame shards back to back
+// ([P][K/P][N][H][d] = [K][N][H][d]).
+static tsf_status block_sim(tsf_handle* h, const tsf_bf16* x, float* y, cudaStream_t st) {
+  const int P = h->world, Nl = h->N / P, Kl = h->K / P, H = h->H, d = h->d;
+  const size_t El = (size_t)h->K * Nl * H * d;            // token shard = frame shard elements
+  const size_t Ey = (size_t)Kl * h->N * H * d;
+  tsf_status s = TSF_ERR_UNSUPPORTED;
+  if (h->fused) {
+    void* peers[MAX_PEERS];
+    for (int r = 0; r < P; ++r) peers[r] = h->uxt + r * El;
+    for (int r = 0; r < P; ++r) {
+      s = temporal_fused(h, temporal_view(h->K, Nl, H, d), x + r * El, r, peers, st);
+      if (s != TSF_OK) break;
+    }
+    if (s == TSF_OK) {
+      for (int r = 0; r < P && s == TSF_OK; ++r) s = spatial_shard(h, h->uxt + r * El, y + r * Ey, 1, 0, false, st);
+      return s;
+    }
+    if (s != TSF_ERR_UNSUPPORTED) return s;
+  }
+  // NCCL byte plan (one head chunk), device copies as the transport
+  for (int r = 0; r < P; ++r)
+    if ((s = temporal_tokens(h, x + r * El, h->xt + r * El, 0, st)) != TSF_OK) return s;
+  {
+    StageTimer tm(h, st, 2);
+    if ((s = exchange_sim(h, h->xt, h->rxt, El, 0, 0, exchange_peer_bytes(h), st)) != TSF_OK) return s;
+    tm.done();
+  }
+  for (int r = 0; r < P; ++r) {
+    if ((s = unpack_chunk(h, h->rxt + r * El, h->uxt + r * El, 0, st)) != TSF_OK) return s;
+    if ((s = spatial_shard(h, h->uxt + r * El, y + r * Ey, 1, 0, true, st)) != TSF_OK) return s;
+  }
   return TSF_OK;
 }
 
@@ -742,10 +924,12 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
   if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
   h->launches = 0;
   const int P = h->world, Nl = h->N / P, Kl = h->K / P;
-  const size_t in_bytes = (size_t)h->K * Nl * h->H * h->d * 2;
-  const size_t out_bytes = (size_t)Kl * h->N * h->H * h->d * 4;
+  const int V = h->sim ? P : 1;  // a simulated handle takes every virtual rank's shard
+  const size_t in_bytes = (size_t)h->K * Nl * h->H * h->d * 2 * V;
+  const size_t out_bytes = (size_t)Kl * h->N * h->H * h->d * 4 * V;
   tsf_status s = check_ptrs(h, {x}, y, in_bytes, out_bytes);
   if (s != TSF_OK) return s;
+  if ((s = check_comm(h)) != TSF_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   if (P == 1) {
     // temporal stage: X_t = x + T(x, x, x), stored fp16
@@ -761,6 +945,7 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
     tm.done();
     return s;
   }
+  if (h->sim) return block_sim(h, x, y, st);
   if (h->fused) {
     // Fused exchange: the temporal kernel writes X_t rows straight into the
     // owning rank's frame shard (CUDA IPC + NVLink TMA/plain stores), a 1-int
@@ -776,20 +961,12 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
     if (nc == 1) {
       void* peers[MAX_PEERS];
       peers_of(0, peers);
-      const DistOut dist{P, Kl, h->rank, Nl, peers};
-      {
-        StageTimer tm(h, st, 0);
-        s = run_attention(h, temporal_view(h->K, Nl, H, d), x, x, x, EPI_BLOCK_T, nullptr, nullptr, st, nullptr,
-                          &dist);
-        tm.done();
-      }
+      s = temporal_fused(h, temporal_view(h->K, Nl, H, d), x, h->rank, peers, st);
       if (s == TSF_OK) {
         StageTimer tm(h, st, 2);
         TSF_NCCL(h, ncclAllReduce(h->d_flag, h->d_flag, 1, ncclInt32, ncclSum, h->comm, st));
         tm.done();
-        StageTimer tm1(h, st, 1);
-        s = run_attention(h, spatial_view(Kl, h->N, H, d), u, u, u, EPI_BLOCK_S, nullptr, y, st);
-        tm1.done();
+        s = spatial_shard(h, u, y, 1, 0, false, st);
         if (s == TSF_OK) h->fparity ^= 1;
         return s;
       }
@@ -802,13 +979,7 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
       for (int c = 0; c < nc && s == TSF_OK; ++c) {
         void* peers[MAX_PEERS];
         peers_of(c, peers);
-        const DistOut dist{P, Kl, h->rank, Nl, peers};
-        const tsf_bf16* xc = x + (size_t)c * Hc * d;
-        {
-          StageTimer tm(h, cs, 0);
-          s = run_attention(h, vin, xc, xc, xc, EPI_BLOCK_T, nullptr, nullptr, cs, nullptr, &dist);
-          tm.done();
-        }
+        s = temporal_fused(h, vin, x + (size_t)c * Hc * d, h->rank, peers, cs);
         if (s != TSF_OK) break;
         StageTimer tm(h, cs, 2);
         TSF_NCCL(h, ncclAllReduce(h->d_flag, h->d_flag, 1, ncclInt32, ncclSum, h->comm, cs));
@@ -816,13 +987,9 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
         TSF_CUDA(h, cudaEventRecord(h->ev_f[c], cs));
       }
       if (s == TSF_OK) {
-        const View vs{h->N, Hc, Kl, (long long)H * d, (long long)d, (long long)h->N * H * d};
         for (int c = 0; c < nc && s == TSF_OK; ++c) {
           TSF_CUDA(h, cudaStreamWaitEvent(st, h->ev_f[c], 0));
-          StageTimer tm(h, st, 1);
-          const __half* uc = u + (size_t)c * Hc * d;
-          s = run_attention(h, vs, uc, uc, uc, EPI_BLOCK_S, nullptr, y + (size_t)c * Hc * d, st, &vs);
-          tm.done();
+          s = spatial_shard(h, u, y, nc, c, false, st);
         }
         if (s == TSF_OK) h->fparity ^= 1;
         return s;
@@ -837,16 +1004,9 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
   // Distributed: head-chunk pipeline.  temporal(c) for all chunks on `st`;
   // exchange(c) on the comm stream after temporal(c); unpack(c) + spatial(c)
   // on `st` after exchange(c), so exchange(c+1) overlaps spatial(c).
-  const int nc = h->nchunk, Hc = h->H / nc, K = h->K, N = h->N, H = h->H, d = h->d;
-  const size_t chunk_elems = (size_t)K * Nl * Hc * d;
+  const int nc = h->nchunk;
   for (int c = 0; c < nc; ++c) {
-    StageTimer tm(h, st, 0);
-    const View vin{K, Hc, Nl, (long long)Nl * H * d, (long long)d, (long long)H * d};
-    const View vout{K, Hc, Nl, (long long)Nl * Hc * d, (long long)d, (long long)Hc * d};
-    const tsf_bf16* xc = x + (size_t)c * Hc * d;
-    s = run_attention(h, vin, xc, xc, xc, EPI_BLOCK_T, h->xt + c * chunk_elems, nullptr, st, &vout);
-    tm.done();
-    if (s != TSF_OK) return s;
+    if ((s = temporal_tokens(h, x, h->xt, c, st)) != TSF_OK) return s;
     TSF_CUDA(h, cudaEventRecord(h->ev_t[c], st));
   }
   for (int c = 0; c < nc; ++c) {
@@ -859,14 +1019,8 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
   }
   for (int c = 0; c < nc; ++c) {
     TSF_CUDA(h, cudaStreamWaitEvent(st, h->ev_a[c], 0));
-    if ((s = unpack_chunk(h, c, st)) != TSF_OK) return s;
-    StageTimer tm(h, st, 1);
-    const __half* u = h->uxt + c * chunk_elems;
-    const View vs{N, Hc, Kl, (long long)Hc * d, (long long)d, (long long)N * Hc * d};
-    const View vy{N, Hc, Kl, (long long)H * d, (long long)d, (long long)N * H * d};
-    s = run_attention(h, vs, u, u, u, EPI_BLOCK_S, nullptr, y + (size_t)c * Hc * d, st, &vy);
-    tm.done();
-    if (s != TSF_OK) return s;
+    if ((s = unpack_chunk(h, h->rxt, h->uxt, c, st)) != TSF_OK) return s;
+    if ((s = spatial_shard(h, h->uxt, y, nc, c, true, st)) != TSF_OK) return s;
   }
   return TSF_OK;
 }
@@ -875,10 +1029,15 @@ tsf_status tsf_spacetime_block_host(tsf_handle* h, const tsf_bf16* x_host, float
   if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
   if (!x_host || !y_host) return fail(h, TSF_ERR_CONFIG, "null host buffer");
   const int P = h->world, Nl = h->N / P, Kl = h->K / P;
-  const size_t in_bytes = (size_t)h->K * Nl * h->H * h->d * 2;
-  const size_t out_bytes = (size_t)Kl * h->N * h->H * h->d * 4;
-  if (!h->xdev) {
-    if (cudaMalloc(&h->xdev, in_bytes) != cudaSuccess || cudaMalloc(&h->ydev, out_bytes) != cudaSuccess) {
+  const int V = h->sim ? P : 1;
+  const size_t in_bytes = (size_t)h->K * Nl * h->H * h->d * 2 * V;
+  const size_t out_bytes = (size_t)Kl * h->N * h->H * h->d * 4 * V;
+  if (!h->xdev || !h->ydev) {  // both or neither: a half-done allocation is undone
+    if (!h->xdev && cudaMalloc(&h->xdev, in_bytes) != cudaSuccess) h->xdev = nullptr;
+    if (h->xdev && !h->ydev && cudaMalloc(&h->ydev, out_bytes) != cudaSuccess) h->ydev = nullptr;
+    if (!h->xdev || !h->ydev) {
+      if (h->xdev) cudaFree(h->xdev);
+      h->xdev = nullptr;
       cudaGetLastError();
       return fail(h, TSF_ERR_NOMEM, "staging cudaMalloc failed");
     }
@@ -927,8 +1086,7 @@ tsf_status tsf_spacetime_block_host(tsf_handle* h, const tsf_bf16* x_host, float
     }
     TSF_CUDA(h, cudaEventRecord(h->ev_h[HOST_CHUNKS], h->copy_stream));
     TSF_CUDA(h, cudaStreamWaitEvent(st, h->ev_h[HOST_CHUNKS], 0));  // the next call's stage buffers
-    TSF_CUDA(h, cudaStreamSynchronize(st));
-    return TSF_OK;
+    return tsf_sync(h, st, 0);
   }
   tsf_status s = tsf_spacetime_block(h, reinterpret_cast<const tsf_bf16*>(h->xdev), h->ydev, stream);
   if (s != TSF_OK) return s;
@@ -937,7 +1095,38 @@ tsf_status tsf_spacetime_block_host(tsf_handle* h, const tsf_bf16* x_host, float
     TSF_CUDA(h, cudaMemcpyAsync(y_host, h->ydev, out_bytes, cudaMemcpyDeviceToHost, st));
     tm.done();
   }
-  TSF_CUDA(h, cudaStreamSynchronize(st));
+  return tsf_sync(h, st, 0);
+}
+
+tsf_status tsf_sync(tsf_handle* h, void* stream, int timeout_ms) {
+  if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
+  cudaStream_t st = (cudaStream_t)stream;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e == cudaSuccess) break;
+    if (e != cudaErrorNotReady) return fail(h, TSF_ERR_CUDA, std::string("stream: ") + cudaGetErrorString(e));
+    tsf_status s = check_comm(h);
+    if (s != TSF_OK) return s;
+    if (timeout_ms > 0) {
+      const double ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      if (ms > timeout_ms) {
+        if (h->comm && !h->sim) {  // a peer is gone or hung: abort so the stream drains
+          ncclCommAbort(h->comm);
+          h->comm = nullptr;
+          h->comm_dead = true;
+        }
+        return fail(h, TSF_ERR_NCCL, "tsf_sync: timeout after " + std::to_string(timeout_ms) + " ms");
+      }
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  if (h->nf_host && *h->nf_host) {
+    *h->nf_host = 0u;
+    return fail(h, TSF_ERR_NUMERIC,
+                "non-finite X_t: |x + T(x)| exceeded the fp16 range of the block intermediate (or x was not finite)");
+  }
   return TSF_OK;
 }
 
@@ -946,9 +1135,10 @@ tsf_status tsf_reshard(tsf_handle* h, int dir, const tsf_bf16* in, tsf_bf16* out
   if (dir != TSF_T2S && dir != TSF_S2T) return fail(h, TSF_ERR_CONFIG, "bad direction");
   h->launches = 0;
   const int P = h->world, Kc = h->K / P, Nc = h->N / P;
-  const size_t bytes = (size_t)h->K * Nc * h->H * h->d * 2;  // same size both ways
-  tsf_status s = check_ptrs(h, {in}, out, bytes, bytes);
+  const size_t bytes = (size_t)h->K * Nc * h->H * h->d * 2;  // same size both ways (one rank)
+  tsf_status s = check_ptrs(h, {in}, out, bytes * (h->sim ? P : 1), bytes * (h->sim ? P : 1));
   if (s != TSF_OK) return s;
+  if ((s = check_comm(h)) != TSF_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   StageTimer tm(h, st, 2);
   if (P == 1) {
@@ -959,32 +1149,51 @@ tsf_status tsf_reshard(tsf_handle* h, int dir, const tsf_bf16* in, tsf_bf16* out
   const size_t chunk = bytes / P;
   const int vecs = h->H * h->d * 2 / 16;
   const long long items = (long long)P * Kc * Nc * vecs;
+  const size_t El = bytes / 2;  // elements of one rank's shard
+  const __half* hin = reinterpret_cast<const __half*>(in);
+  __half* hout = reinterpret_cast<__half*>(out);
+  const int V = h->sim ? P : 1;  // ranks handled by this call
   if (dir == TSF_T2S) {
     // send frames [p Kc, (p+1) Kc) of the token shard (contiguous); receive
     // [P][Kc][Nc] blocks, unpack to [Kc][N]
-    TSF_NCCL(h, ncclGroupStart());
-    for (int p = 0; p < P; ++p) {
-      TSF_NCCL(h, ncclSend((const char*)in + p * chunk, chunk, ncclUint8, p, h->comm, st));
-      TSF_NCCL(h, ncclRecv((char*)h->rxt + p * chunk, chunk, ncclUint8, p, h->comm, st));
+    if (h->sim) {
+      if ((s = exchange_sim(h, hin, h->rxt, El, 0, 0, chunk, st)) != TSF_OK) return s;
+    } else {
+      TSF_NCCL(h, ncclGroupStart());
+      for (int p = 0; p < P; ++p) {
+        TSF_NCCL(h, ncclSend((const char*)in + p * chunk, chunk, ncclUint8, p, h->comm, st));
+        TSF_NCCL(h, ncclRecv((char*)h->rxt + p * chunk, chunk, ncclUint8, p, h->comm, st));
+      }
+      TSF_NCCL(h, ncclGroupEnd());
     }
-    TSF_NCCL(h, ncclGroupEnd());
-    reshard_perm_kernel<true><<<grid_for(h, items), 256, 0, st>>>((const uint4*)h->rxt, (uint4*)out, nullptr,
-                                                                  nullptr, P, Kc, Nc, vecs);
+    for (int r = 0; r < V; ++r) {
+      reshard_perm_kernel<true><<<grid_for(h, items), 256, 0, st>>>((const uint4*)(h->rxt + r * El),
+                                                                    (uint4*)(hout + r * El), nullptr, nullptr, P,
+                                                                    Kc, Nc, vecs);
+      h->launches++;
+    }
   } else {
     // pack [Kc][N] -> [P][Kc][Nc], send block p to peer p; the received
     // blocks [P][Kc][Nc] are exactly the token shard [K][Nc]
-    reshard_perm_kernel<false><<<grid_for(h, items), 256, 0, st>>>((const uint4*)in, (uint4*)h->rxt, nullptr,
-                                                                   nullptr, P, Kc, Nc, vecs);
-    TSF_CUDA(h, cudaGetLastError());
-    TSF_NCCL(h, ncclGroupStart());
-    for (int p = 0; p < P; ++p) {
-      TSF_NCCL(h, ncclSend((const char*)h->rxt + p * chunk, chunk, ncclUint8, p, h->comm, st));
-      TSF_NCCL(h, ncclRecv((char*)out + p * chunk, chunk, ncclUint8, p, h->comm, st));
+    for (int r = 0; r < V; ++r) {
+      reshard_perm_kernel<false><<<grid_for(h, items), 256, 0, st>>>((const uint4*)(hin + r * El),
+                                                                     (uint4*)(h->rxt + r * El), nullptr, nullptr,
+                                                                     P, Kc, Nc, vecs);
+      h->launches++;
     }
-    TSF_NCCL(h, ncclGroupEnd());
+    TSF_CUDA(h, cudaGetLastError());
+    if (h->sim) {
+      if ((s = exchange_sim(h, h->rxt, hout, El, 0, 0, chunk, st)) != TSF_OK) return s;
+    } else {
+      TSF_NCCL(h, ncclGroupStart());
+      for (int p = 0; p < P; ++p) {
+        TSF_NCCL(h, ncclSend((const char*)h->rxt + p * chunk, chunk, ncclUint8, p, h->comm, st));
+        TSF_NCCL(h, ncclRecv((char*)out + p * chunk, chunk, ncclUint8, p, h->comm, st));
+      }
+      TSF_NCCL(h, ncclGroupEnd());
+    }
   }
   TSF_CUDA(h, cudaGetLastError());
-  h->launches++;
   tm.done();
   return TSF_OK;
 }

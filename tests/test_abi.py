@@ -72,3 +72,27 @@ def test_oracle_and_product_are_independent():
     for root, _, files in os.walk(os.path.join(ROOT, "paper_2604_16590_b200", "csrc")):
         for f in files:
             assert "oracle" not in open(os.path.join(root, f)).read().lower() or f.endswith(".md")
+
+
+def test_distributed_create_rejects_mismatched_world_without_collectives():
+    """Fault injection on the distributed boundary: a world size the shape cannot
+    shard, a rank outside the world, or a simulated world beyond one box fail
+    synchronously with TSF_ERR_CONFIG before any device work or NCCL collective
+    (so a misconfigured rank cannot leave its peers waiting in a collective)."""
+    import ctypes
+    import paper_2604_16590_b200 as tsf
+    L = tsf.lib()
+    h = ctypes.c_void_p()
+    uid = (ctypes.c_char * 128)()
+    assert L.tsf_create_dist(6, 64, 2, 64, uid, 0, 4, ctypes.byref(h)) == tsf.TSF_ERR_CONFIG   # K % P
+    assert b"divisible" in L.tsf_last_error(None)
+    assert L.tsf_create_dist(8, 66, 2, 64, uid, 0, 4, ctypes.byref(h)) == tsf.TSF_ERR_CONFIG   # N % P
+    assert L.tsf_create_dist(8, 64, 2, 64, uid, 4, 4, ctypes.byref(h)) == tsf.TSF_ERR_CONFIG   # rank >= world
+    assert L.tsf_create_dist(8, 64, 2, 64, uid, -1, 4, ctypes.byref(h)) == tsf.TSF_ERR_CONFIG
+    assert L.tsf_create_dist(8, 64, 2, 48, uid, 0, 4, ctypes.byref(h)) == tsf.TSF_ERR_UNSUPPORTED
+    assert L.tsf_create_sim(8, 64, 2, 64, 16, 2, ctypes.byref(h)) == tsf.TSF_ERR_CONFIG       # P > 8
+    assert L.tsf_create_sim(8, 64, 2, 64, 4, 3, ctypes.byref(h)) == tsf.TSF_ERR_CONFIG        # bad mode
+    assert L.tsf_create_sim(6, 64, 2, 64, 4, 2, ctypes.byref(h)) == tsf.TSF_ERR_CONFIG        # K % P
+    assert not h.value
+    assert L.tsf_world_size(None) == -1
+    assert L.tsf_sync(None, None, 0) == tsf.TSF_ERR_CONFIG

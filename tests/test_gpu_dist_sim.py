@@ -1,0 +1,111 @@
+"""The distributed block (the token->frame exchange) on ONE
+GPU: tsf_create_sim runs P virtual ranks with the distributed path's own code
+(output routing by frame l -> rank l / (K/P), b_off, per-destination tensor
+maps, the flash kernel's staged peer-row epilogue, the NCCL byte plan and the
+unpack kernel); only the transport is local.
+
+Bar (BASELINE.json north_star): "the all-to-all reshard must be bit-exact".
+  * y of the P-rank block == y of the single-GPU block, bitwise (the
+    exchange moves fp16 X_t bytes untouched, and every group is computed by
+    the same kernel tile either way);
+  * y matches the fp64 oracle on sampled rows within the
+    north-star tolerance;
+  * tsf_reshard T2S / S2T equal the index permutation of oracle.shard_* (O5).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS, REL_L2 = 2e-2, 1e-2
+
+
+def stack_token_shards(xb, P):
+    K, N, H, d = xb.shape
+    Nl = N // P
+    return np.ascontiguousarray(np.stack([xb[:, r * Nl:(r + 1) * Nl] for r in range(P)]))
+
+
+def sampled_rows(K, N, H, n, seed):
+    g = np.random.default_rng(seed)
+    rows = {(int(g.integers(K)), int(g.integers(N)), int(g.integers(H))) for _ in range(n)}
+    return sorted(rows | {(0, 0, 0), (K - 1, N - 1, H - 1)})
+
+
+# (K, N, H, d) per P.  Temporal kernel of each: packed (K <= 128) or flash (K > 128).
+def cases():
+    out = []
+    for P in (2, 4, 8):
+        out += [
+            pytest.param(P, (8 * P, 4096, 16, 64), id=f"P{P}-C2weak-packed"),    # bench.py --gpus P (weak, C2/GPU)
+            pytest.param(P, (200, 8 * P, 2, 64), id=f"P{P}-K200-flash"),         # staged peer rows (flash temporal)
+            pytest.param(P, (128, 32 * P, 2, 128), id=f"P{P}-K128-d128"),        # C4-at-P=8 temporal shape
+        ]
+    out.append(pytest.param(4, (12, 96, 3, 32), id="P4-d32-ragged"))
+    return out
+
+
+@pytest.fixture(scope="module")
+def single_cache():
+    return {}
+
+
+@pytest.mark.parametrize("mode", [2, 1], ids=["fused", "nccl-plan"])
+@pytest.mark.parametrize("P,shape", cases())
+def test_sim_block_bitwise_equals_single_gpu(tsf_lib, single_cache, P, shape, mode):
+    K, N, H, d = shape
+    xb = synth.make_x(K, N, H, d, seed=21)
+    key = (shape,)
+    if key not in single_cache:
+        one = tsf_lib.Layer(K, N, H, d)
+        single_cache[key] = one.block(synth.bits_to_torch(xb, "cuda")).cpu()
+        one.close()
+    y1 = single_cache[key]
+    sim = tsf_lib.Layer(K, N, H, d, sim_world=P, sim_mode=mode)
+    assert sim.exchange_mode() == mode
+    xs = synth.bits_to_torch(stack_token_shards(xb, P), "cuda")
+    y = sim.block(xs)
+    sim.sync()
+    y = y.reshape(K, N, H, d).cpu()
+    assert torch.equal(y, y1), (f"P={P} mode={mode}: max |dy| = "
+                                f"{(y - y1).abs().max().item():.3e} (must be bitwise equal)")
+    # oracle parity on sampled rows of the P-rank result itself
+    rows = sampled_rows(K, N, H, 96, seed=P)
+    want = oracle.block_rows(synth.bf16_bits_to_f64(xb), rows)
+    ri = torch.tensor(rows)
+    got = y[ri[:, 0], ri[:, 1], ri[:, 2]].double().numpy()
+    err = np.abs(got - want)
+    rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+    print(f"P={P} mode={mode} {shape}: max-abs {err.max():.3e} rel-L2 {rel:.3e} max|ref| {np.abs(want).max():.2f}")
+    assert err.max() <= MAX_ABS and rel <= REL_L2
+    sim.close()
+
+
+@pytest.mark.parametrize("P,shape", [(2, (8, 64, 2, 64)), (4, (8, 96, 3, 32)), (8, (16, 64, 2, 128))])
+def test_sim_reshard_is_the_index_permutation(tsf_lib, P, shape):
+    """I10: T2S equals oracle.reshard_t2s of the token shards; S2T o T2S = id (bitwise)."""
+    K, N, H, d = shape
+    xb = synth.make_x(K, N, H, d, seed=22)
+    sim = tsf_lib.Layer(K, N, H, d, sim_world=P, sim_mode=1)
+    xs_np = stack_token_shards(xb, P)
+    xs = synth.bits_to_torch(xs_np, "cuda")
+    fr = sim.reshard(xs, tsf_lib.TSF_T2S)
+    back = sim.reshard(fr, tsf_lib.TSF_S2T)
+    torch.cuda.synchronize()
+    want = oracle.reshard_t2s([xs_np[r] for r in range(P)])
+    assert torch.equal(fr.cpu(), synth.bits_to_torch(np.ascontiguousarray(np.stack(want))))
+    assert torch.equal(back, xs)
+    sim.close()
+
+
+def test_sim_handle_rejects_bad_world(tsf_lib):
+    with pytest.raises(tsf_lib.TsfError) as e:
+        tsf_lib.Layer(6, 64, 2, 64, sim_world=4)      # K % P != 0
+    assert e.value.status == tsf_lib.TSF_ERR_CONFIG
+    with pytest.raises(tsf_lib.TsfError) as e:
+        tsf_lib.Layer(8, 64, 2, 64, sim_world=16)     # beyond the 8 GPUs of a box
+    assert e.value.status == tsf_lib.TSF_ERR_CONFIG

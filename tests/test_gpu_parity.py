@@ -5,6 +5,8 @@ Bar (BASELINE.json north_star): max-abs error <= 2e-2 and relative L2 error
 several 128-row tiles with ragged tails; the full BASELINE sizes are checked on
 sampled rows and full (t, h) planes the oracle computes one by one.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -26,9 +28,17 @@ def f64(bits):
 
 
 def check(got, want, what):
+    """Gate + margin log: every case prints (and, with TSF_PARITY_LOG set, appends
+    to that file) max-abs, rel-L2 and max|ref| so the margin to the gate is visible."""
     got = np.asarray(got, dtype=np.float64)
     err = np.abs(got - want)
     rel = np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30)
+    line = (f"{what}: max-abs {err.max():.3e} ({err.max() / MAX_ABS:.0%} of gate)  rel-L2 {rel:.3e} "
+            f"({rel / REL_L2:.0%} of gate)  max|ref| {np.abs(want).max():.2f}  n={got.size}")
+    print(line)
+    if os.environ.get("TSF_PARITY_LOG"):
+        with open(os.environ["TSF_PARITY_LOG"], "a") as f:
+            f.write(line + "\n")
     assert np.all(np.isfinite(got)), f"{what}: non-finite output"
     assert err.max() <= MAX_ABS and rel <= REL_L2, \
         f"{what}: max-abs {err.max():.3e} rel-L2 {rel:.3e} (max|ref| {np.abs(want).max():.2f})"
@@ -54,6 +64,9 @@ ATTN_SHAPES = [
     (2, 100, 4, 32),     # spatial packed N=100 (WIN=128)
     (8, 1000, 40, 64),   # spatial flash with ~4 work items per persistent CTA (Q/S/P buffer reuse)
     (300, 8, 64, 32),    # temporal flash d=32 with several work items per CTA
+    (128, 40, 2, 128),   # temporal packed K=128 at d=128 (the C4-at-P=8 temporal shape)
+    (200, 4, 2, 128),    # temporal flash at d=128 (K > 128)
+    (3, 300, 2, 32),     # spatial flash at d=32 (N > 128), ragged
 ]
 
 
@@ -205,13 +218,60 @@ def test_abi_errors(tsf_lib):
     assert b"aligned" in L.tsf_last_error(layer._h)
 
 
-def test_full_C2_block_every_row(tsf_lib):
-    """The bench workload (BASELINE configs[1]) compared on EVERY output element."""
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])
+def test_full_C2_block_every_row(tsf_lib, seed):
+    """The bench workload (BASELINE configs[1]) compared on EVERY output element,
+    data seeds 0-4."""
     w = synth.CONFIGS["C2"]
-    xb = synth.make_x(w.K, w.N, w.H, w.d, seed=0)
+    xb = synth.make_x(w.K, w.N, w.H, w.d, seed=seed)
     layer = tsf_lib.Layer(w.K, w.N, w.H, w.d)
     y = host(layer.block(to_dev(xb)))
-    check(y, oracle.block(f64(xb)), "C2 block, all rows")
+    check(y, oracle.block(f64(xb)), f"C2 block seed {seed}, all rows")
+
+
+def scaled_bits(bits, factor):
+    """bf16 bits times a power of two (exact in bf16)."""
+    return synth.f64_to_bf16_bits(synth.bf16_bits_to_f64(bits) * factor)
+
+
+@pytest.mark.parametrize("factor", [2.0, 4.0])
+def test_block_large_magnitude_x(tsf_lib, factor):
+    """x scaled by 2 / 4 (|x| <= 8 / 16): logits 4x / 16x larger (peaky softmax in
+    both stages) and |X_t|, |y| several times the default; shows the real margin."""
+    K, N, H, d = 8, 1000, 4, 64
+    xb = scaled_bits(synth.make_x(K, N, H, d, seed=6), factor)
+    layer = tsf_lib.Layer(K, N, H, d)
+    y = host(layer.block(to_dev(xb)))
+    check(y, oracle.block(f64(xb)), f"block x*{factor:g} {(K, N, H, d)}")
+
+
+def test_block_nonfinite_x_t_is_reported(tsf_lib):
+    """|x| = 4e4: X_t = x + T(x) ~ 8e4 exceeds fp16 -> TSF_ERR_NUMERIC, not silent inf."""
+    K, N, H, d = 4, 64, 2, 32
+    layer = tsf_lib.Layer(K, N, H, d)
+    x = torch.full((K, N, H, d), 4.0e4, dtype=torch.bfloat16, device="cuda")
+    layer.block(x)
+    with pytest.raises(tsf_lib.TsfError) as e:
+        layer.sync()
+    assert e.value.status == tsf_lib.TSF_ERR_NUMERIC
+    layer.sync()                                   # the flag was cleared
+    # the host API synchronises and reports it directly
+    xh = x.cpu().pin_memory()
+    yh = torch.empty((K, N, H, d), dtype=torch.float32).pin_memory()
+    with pytest.raises(tsf_lib.TsfError) as e:
+        layer.block_host(xh, yh)
+    assert e.value.status == tsf_lib.TSF_ERR_NUMERIC
+    # in range: no error (|x| = 1e4 -> X_t = 2e4 < 65504)
+    layer.block(torch.full((K, N, H, d), 1.0e4, dtype=torch.bfloat16, device="cuda"))
+    layer.sync()
+    # a flash-kernel temporal stage (K > 128) reports it too
+    big = tsf_lib.Layer(200, 2, 2, 64)
+    xb = torch.zeros((200, 2, 2, 64), dtype=torch.bfloat16, device="cuda")
+    xb[7, 1, 1, 5] = float("inf")
+    big.block(xb)
+    with pytest.raises(tsf_lib.TsfError) as e:
+        big.sync()
+    assert e.value.status == tsf_lib.TSF_ERR_NUMERIC
 
 
 @pytest.mark.parametrize("cfg,K", [("C3", 32), ("C4", 4)])
@@ -227,6 +287,8 @@ def test_large_config_block_sampled(tsf_lib, cfg, K):
     yi = torch.tensor(rows, dtype=torch.long)
     got = y[yi[:, 0], yi[:, 1], yi[:, 2]].double().cpu().numpy()
     check(got, oracle.block_rows(x, rows), f"{cfg} (K={K}) block sampled rows")
+    if cfg == "C3":   # one full (t, h) plane: all N = 16384 tokens of frame 17, head 5
+        check(y[17, :, 5].double().cpu().numpy(), oracle.block_plane(x, 17, 5), "C3 block plane (17,5)")
 
 
 def test_c_abi_program(tsf_lib, tmp_path):

@@ -1,6 +1,6 @@
 // Probe: does tcgen05.mma kind::f16 accept A = fp16 with B = bf16 (mixed
 // formats in the instruction descriptor)?  D[128x16] = A[128x64] * B[16x64]^T.
-// Build: nvcc -gencode arch=compute_100a,code=sm_100a -I paper_2604_16590_b200/csrc tools/mma_mixed_test.cu
+// Build: nvcc -cudart shared -gencode arch=compute_100a,code=sm_100a -I paper_2604_16590_b200/csrc tools/mma_mixed_test.cu
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>

@@ -1,7 +1,7 @@
 // Microbenchmark of the softmax instruction mix on sm_100a: issue cost per
 // warp-instruction per SM sub-partition for MUFU.EX2 (f32, f16x2), F2FP
 // packing, FFMA2, FMNMX3 and the polynomial exp2.  One CTA, W warps.
-// nvcc -gencode arch=compute_100a,code=sm_100a -I paper_2604_16590_b200/csrc tools/ubench.cu -o tools/ubench
+// nvcc -cudart shared -gencode arch=compute_100a,code=sm_100a -I paper_2604_16590_b200/csrc tools/ubench.cu -o tools/ubench
 #include <cstdio>
 #include <cuda_fp16.h>
 #include "sm100.cuh"

@@ -1,6 +1,6 @@
 // Which pipe does F2FP (fp32 pair -> packed 16-bit) share with MUFU.EX2?
 // Independent streams, 2 warps per SMSP; cycles per inner iteration.
-// nvcc -gencode arch=compute_100a,code=sm_100a -I paper_2604_16590_b200/csrc tools/ubench2.cu -o tools/ubench2
+// nvcc -cudart shared -gencode arch=compute_100a,code=sm_100a -I paper_2604_16590_b200/csrc tools/ubench2.cu -o tools/ubench2
 #include <cstdio>
 #include <cuda_fp16.h>
 #include "sm100.cuh"

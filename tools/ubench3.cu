@@ -1,6 +1,6 @@
 // TMEM load/store throughput on sm_100a: W warps each issue tcgen05.ld/st
 // 32x32b.x32 (4 KB per warp-instruction) in a loop.  Prints bytes/clk/SM.
-// nvcc -gencode arch=compute_100a,code=sm_100a -I paper_2604_16590_b200/csrc tools/ubench3.cu -o tools/ubench3
+// nvcc -cudart shared -gencode arch=compute_100a,code=sm_100a -I paper_2604_16590_b200/csrc tools/ubench3.cu -o tools/ubench3
 #include <cstdio>
 #include "sm100.cuh"
 using namespace tsf;

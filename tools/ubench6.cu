@@ -4,7 +4,7 @@
 // three-pass structure as attn_flash.cuh.  Reports cycles per 128-column row
 // per warp with W warps on each SM sub-partition (W = 1: ping-pong, one
 // warpgroup at a time; W = 2: both softmax warpgroups at once).
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2604_16590_b200/csrc tools/ubench6.cu -o tools/ubench6
+// nvcc -cudart shared -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2604_16590_b200/csrc tools/ubench6.cu -o tools/ubench6
 #include <cstdio>
 #include <cuda_fp16.h>
 #include "sm100.cuh"
