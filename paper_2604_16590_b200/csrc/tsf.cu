@@ -19,6 +19,7 @@
 
 #include "attn_flash.cuh"
 #include "attn_packed.cuh"
+#include "attn_stream.cuh"
 #include "layout.cuh"
 
 using namespace tsf;
@@ -322,10 +323,40 @@ static tsf_status launch_flash_t(tsf_handle* h, cudaStream_t st, const CUtensorM
   return launch_flash_emu<D, EPI, 0>(h, st, mq, mk, mv, p);
 }
 
+// Streaming block temporal stage (attn_stream.cuh): d in {32, 64}, window 32 / 64.
+// TSF_STREAM=0 selects the older one-slot packed kernel (A/B measurements).
+static bool use_stream(int d, int win) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("TSF_STREAM");
+    env = e ? atoi(e) : 1;
+  }
+  return env != 0 && (d == 32 || d == 64) && (win == 32 || win == 64);
+}
+
+template <int D, int WIN>
+static tsf_status launch_stream_t(tsf_handle* h, cudaStream_t st, const CUtensorMap& mx, const CUtensorMap& mo,
+                                  const AttnParams& p) {
+  if constexpr (D <= 64 && WIN <= 64) {
+    constexpr int NST = 8;
+    using C = StreamCfg<D, WIN, NST>;
+    int grid = h->num_sms;
+    if (grid > p.num_tiles) grid = p.num_tiles;
+    return launch(h, attn_stream_kernel<D, WIN, NST>, grid, C::THREADS, C::SMEM, st, p, mx, mo, h->pm);
+  }
+  return fail(h, TSF_ERR_UNSUPPORTED, "stream kernel shape");
+}
+
 template <int D, int EPI, bool SHARED>
 static tsf_status dispatch_packed_win(tsf_handle* h, int win, cudaStream_t st, const CUtensorMap& mq,
                                       const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mo,
                                       const AttnParams& p) {
+  if constexpr (EPI == EPI_BLOCK_T && D <= 64) {
+    if (use_stream(D, win)) {
+      if (win == 32) return launch_stream_t<D, 32>(h, st, mq, mo, p);
+      return launch_stream_t<D, 64>(h, st, mq, mo, p);
+    }
+  }
   switch (win) {
     case 32: return launch_packed_t<D, 32, EPI, SHARED>(h, st, mq, mk, mv, mo, p);
     case 64: return launch_packed_t<D, 64, EPI, SHARED>(h, st, mq, mk, mv, mo, p);
