@@ -55,6 +55,15 @@ typedef enum {
 
 enum { TSF_T2S = 0, TSF_S2T = 1 }; /* reshard directions */
 
+/* masks of tsf_joint_attn over the flattened tokens (t, n) -> t*N + n */
+enum {
+  TSF_MASK_NONE = 0,          /* global attention over all K*N tokens (Table I "ViT (global)" P:73) */
+  TSF_MASK_TEMPORAL = 1,      /* [n' == n]: equals tsf_temporal_attn (block-mask check, pin I1) */
+  TSF_MASK_SPATIAL = 2,       /* [t' == t]: equals tsf_spatial_attn (pin I1) */
+  TSF_MASK_CAUSAL_FRAMES = 3  /* [t' <= t]: causal in time, global in space (SURVEY NEXT-4 variant;
+                                 the paper's temporal context is non-causal) */
+};
+
 /* Create a single-GPU handle for a [K, N, H, d] layer on the current CUDA
  * device.  K, N, H >= 1; d in {32, 64, 128}.  Allocates the block workspace
  * (X_t in fp16, 2*K*N*H*d bytes). */
@@ -72,6 +81,19 @@ tsf_status tsf_temporal_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k
  * q, k, v, o: bf16 [Kl, N, H, d] with Kl = K or K/P (the rank's frame shard). */
 tsf_status tsf_spatial_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v,
                             tsf_bf16* o, void* stream);
+
+/* Joint (global) attention over all L = K*N tokens of each head -- the
+ * O((K N)^2) regime the factorization avoids (Table I):
+ *   o[i,h,:] = sum_j softmax_j(<q[i,h,:], k[j,h,:]> / sqrt(d) + M[i,j]) v[j,h,:],
+ * i, j over the flattened tokens (t, n) -> t*N + n, M = 0 where the mask
+ * allows and -inf elsewhere (mask = TSF_MASK_*).  Every score is computed
+ * (masked tiles are not skipped: this is the cost the factorization removes);
+ * with TSF_MASK_TEMPORAL / _SPATIAL the result equals the factorized stages
+ * (a GPU-side block-mask check).  q, k, v, o: bf16 [K, N, H, d]; fp32
+ * accumulation; o rounded to bf16.  Single-GPU handles only
+ * (TSF_ERR_UNSUPPORTED otherwise); K*N < 2^31. */
+tsf_status tsf_joint_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v, tsf_bf16* o,
+                          int mask, void* stream);
 
 /* Divided space-time block, temporal then spatial ("followed by"), with
  * identity projections and residual weight 1 (readings G1, G5):
@@ -175,7 +197,8 @@ int tsf_world_size(const tsf_handle* h);
  * records), 0 stops.  tsf_stage_ms synchronises on the recorded events and
  * returns the summed milliseconds and the number of recorded launches of
  * stage 0 = temporal attention, 1 = spatial attention, 2 = reshard
- * (all-to-all + unpack), 3 = host<->device copies, 4 = tsf_transpose. */
+ * (all-to-all + unpack), 3 = host<->device copies, 4 = tsf_transpose,
+ * 5 = tsf_joint_attn. */
 tsf_status tsf_set_timing(tsf_handle* h, int enable);
 tsf_status tsf_stage_ms(tsf_handle* h, int stage, float* total_ms, int* n_records);
 

@@ -27,6 +27,8 @@ from .attention import (  # noqa: F401
     joint_masked,
     mask_temporal,
     mask_spatial,
+    mask_causal_frames,
+    joint_rows,
     temporal_rows,
     spatial_rows,
     block_rows,

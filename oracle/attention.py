@@ -131,6 +131,17 @@ def mask_spatial(K: int, N: int) -> np.ndarray:
     return t[:, None] == t[None, :]
 
 
+def mask_causal_frames(K: int, N: int) -> np.ndarray:
+    """M_C[(t,n), (t',n')] = [t' <= t]: every token of frames up to its own.
+
+    Not the paper's regime (temporal context = frames modelled jointly,
+    not autoregressive steps); the causal-temporal variant of SURVEY 8(f)
+    NEXT-4, a mask over the same global attention.
+    """
+    t = np.repeat(np.arange(K), N)
+    return t[None, :] <= t[:, None]
+
+
 def joint_masked(q: np.ndarray, k: np.ndarray, v: np.ndarray,
                  mask: np.ndarray | None = None) -> np.ndarray:
     """Attention of every token over all L = K*N tokens, per head.
@@ -148,6 +159,21 @@ def joint_masked(q: np.ndarray, k: np.ndarray, v: np.ndarray,
     P = softmax_rows(S)
     o = np.matmul(P, f(v))
     return o.transpose(1, 0, 2).reshape(K, N, H, d).copy()
+
+
+def joint_rows(q, k, v, rows: Iterable[Sequence[int]], causal_frames: bool = False) -> np.ndarray:
+    """Rows (t, n, h) of joint_masked(q, k, v, None or mask_causal_frames),
+    one by one (any size): row (t, n) attends to all K*N tokens of head h, or
+    to the tokens of frames t' <= t.  -> [R, d]"""
+    _check(q, k, v)
+    K, N, H, d = q.shape
+    out = []
+    for t, n, h in rows:
+        kf = t + 1 if causal_frames else K
+        Kt = k[:kf, :, h].reshape(kf * N, d)
+        V = v[:kf, :, h].reshape(kf * N, d)
+        out.append(attend(q[t, n, h][None], Kt, V)[0])
+    return np.array(out)
 
 
 # ---------------------------------------------------------------------------

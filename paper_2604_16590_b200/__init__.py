@@ -29,7 +29,8 @@ TSF_OK, TSF_ERR_CONFIG, TSF_ERR_NUMERIC, TSF_ERR_UNSUPPORTED, TSF_ERR_CUDA, TSF_
 STATUS_NAMES = {0: "TSF_OK", 2: "TSF_ERR_CONFIG", 3: "TSF_ERR_NUMERIC", 4: "TSF_ERR_UNSUPPORTED",
                 5: "TSF_ERR_CUDA", 6: "TSF_ERR_NCCL", 7: "TSF_ERR_NOMEM"}
 TSF_T2S, TSF_S2T = 0, 1
-STAGE_TEMPORAL, STAGE_SPATIAL, STAGE_RESHARD, STAGE_COPY, STAGE_TRANSPOSE = 0, 1, 2, 3, 4
+TSF_MASK_NONE, TSF_MASK_TEMPORAL, TSF_MASK_SPATIAL, TSF_MASK_CAUSAL_FRAMES = 0, 1, 2, 3
+STAGE_TEMPORAL, STAGE_SPATIAL, STAGE_RESHARD, STAGE_COPY, STAGE_TRANSPOSE, STAGE_JOINT = 0, 1, 2, 3, 4, 5
 
 # Every function declared in include/tsf.h: (name, restype, argtypes)
 _P, _I, _F = ctypes.c_void_p, ctypes.c_int, ctypes.c_float
@@ -37,6 +38,7 @@ SIGNATURES = [
     ("tsf_create", _I, [_I, _I, _I, _I, ctypes.POINTER(_P)]),
     ("tsf_temporal_attn", _I, [_P, _P, _P, _P, _P, _P]),
     ("tsf_spatial_attn", _I, [_P, _P, _P, _P, _P, _P]),
+    ("tsf_joint_attn", _I, [_P, _P, _P, _P, _P, _I, _P]),
     ("tsf_spacetime_block", _I, [_P, _P, _P, _P]),
     ("tsf_spacetime_block_host", _I, [_P, _P, _P, _P]),
     ("tsf_destroy", None, [_P]),
@@ -189,6 +191,19 @@ class Layer:
         _need(out, torch.bfloat16, shp, "out")
         _check(lib().tsf_spatial_attn(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                                       _stream_ptr(stream)), self._h)
+        return out
+
+    def joint(self, q, k, v, mask: int = TSF_MASK_NONE, out=None, stream=None):
+        """tsf_joint_attn: global attention over all K*N tokens (bf16 [K, N, H, d]), O((KN)^2),
+        with an optional TSF_MASK_* (temporal / spatial block mask, causal frames)."""
+        import torch
+        shp = (self.K, self.N, self.H, self.d)
+        for t, n in ((q, "q"), (k, "k"), (v, "v")):
+            _need(t, torch.bfloat16, shp, n)
+        out = torch.empty_like(q) if out is None else out
+        _need(out, torch.bfloat16, shp, "out")
+        _check(lib().tsf_joint_attn(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), int(mask),
+                                    _stream_ptr(stream)), self._h)
         return out
 
     def block(self, x, out=None, stream=None):

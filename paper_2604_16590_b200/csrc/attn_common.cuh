@@ -82,6 +82,10 @@ struct AttnParams {
   // stored fp16 X_t element is +-inf or NaN (|x + T(x)| beyond the fp16 range,
   // or a non-finite input); reported as TSF_ERR_NUMERIC by tsf_sync
   unsigned int* nonfinite;
+  // joint attention over all K*N tokens (tsf_joint_attn, flash kernel MASK = 1):
+  // mask_mode 1 = temporal block mask [n' = n], 2 = spatial block mask
+  // [t' = t], 3 = causal frames [t' <= t]; mask_n = N tokens per frame
+  int mask_mode, mask_n;
 };
 constexpr int FLASH_PINGPONG = 2;
 constexpr int FLASH_RES_GLOBAL = 4;  // flash kernel: block residual from global memory, not the Q tile (diagnostics)

@@ -104,7 +104,7 @@ struct FlashCfg {
   static constexpr int REG_SOFTMAX = SPLIT == 1 ? 224 : 104, REG_PRODUCER = SPLIT == 1 ? 56 : 48;
 };
 
-template <int D, int EPI, int NST, int EMU, int SUB, int SPLIT>
+template <int D, int EPI, int NST, int EMU, int SUB, int SPLIT, int MASK = 0>
 __global__ void __launch_bounds__(FlashCfg<D, EPI, NST, SUB, SPLIT>::THREADS, 1)
 attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                   const __grid_constant__ CUtensorMap tv, const AttnParams p) {
@@ -430,6 +430,35 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
 #pragma unroll
           for (int c = 0; c < CW; ++c) sv[c] = (c < valid) ? sv[c] : 0xFF800000u;  // -inf
         }
+        if constexpr (MASK) {
+          // joint attention over the flattened tokens j = t' N + n' (tsf_joint_attn):
+          // query qi = t N + n, key j of this tile = j0 + c
+          const int Nf = p.mask_n;
+          const int qi = qp * 256 + t * 128 + (int)row;
+          const int ti = qi / Nf, ni = qi - ti * Nf;
+          const int j0 = i * SUB + hf * CW;
+          if (p.mask_mode == 1) {  // [n' = n]: keys j0 + c with (j0 + c - ni) % Nf == 0
+            int first = (ni - j0) % Nf;
+            if (first < 0) first += Nf;
+            uint32_t b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+            for (int c = first; c < CW; c += Nf) {
+              const uint32_t bit = 1u << (c & 31);
+              if (c < 32) b0 |= bit;
+              else if (c < 64) b1 |= bit;
+              else if (c < 96) b2 |= bit;
+              else b3 |= bit;
+            }
+#pragma unroll
+            for (int c = 0; c < CW; ++c) {
+              const uint32_t w = c < 32 ? b0 : c < 64 ? b1 : c < 96 ? b2 : b3;
+              sv[c] = ((w >> (c & 31)) & 1u) ? sv[c] : 0xFF800000u;
+            }
+          } else {  // 2: [t' = t] -> j in [ti Nf, ti Nf + Nf);  3: [t' <= t] -> j < (ti + 1) Nf
+            const int lo = (p.mask_mode == 2 ? ti * Nf : 0) - j0, hi = (ti + 1) * Nf - j0;
+#pragma unroll
+            for (int c = 0; c < CW; ++c) sv[c] = (c >= lo && c < hi) ? sv[c] : 0xFF800000u;
+          }
+        }
         // row max: 8 independent FMNMX3 chains
         float m8[8];
 #pragma unroll
@@ -473,6 +502,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         } else if (__any_sync(0xffffffffu, (m_new - m_run) > RESCALE_LOG2)) {
           rescale = true;
           alpha = ex2(m_run - m_new);
+          if constexpr (MASK) alpha = (m_new == -INFINITY) ? 1.f : alpha;  // row still fully masked
           l_run *= alpha;
           m_run = m_new;
         }
@@ -506,7 +536,9 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         // ping-pong: the two tiles' warps take turns for the exponential phase
         // (MUFU-bound), so one's exps overlap the other's waits / max / stores
         if (pingpong && !(t == 0 && G == 0)) named_bar_sync(1 + t, 256 * SPLIT);
-        const float nmb = -m_run;
+        // a row whose keys so far are all masked (MASK only) has m_run = -inf:
+        // its scores are all -inf and exponentiate against 0 to exactly 0
+        const float nmb = (MASK && m_run == -INFINITY) ? 0.f : -m_run;
         float ls0 = 0.f, ls1 = 0.f;
         // SEP: all of P_t is packed in registers and stored after the last
         // exponential, so the wait for PV_t(G-1) (P_t's buffer) is at the end

@@ -115,6 +115,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
         const int tile = blockIdx.x + i * gridDim.x;
         const int s = i % NST;
         if (i >= NST) mbar_wait_sleep(&in_empty[s], ((i / NST) - 1) & 1);
+        TSF_STAMP(p, C::W_TMA, i);
         const int a0 = (tile % p.tiles_a) * p.Ab, b0 = (tile / p.tiles_a) * p.Bb;
         mbar_arrive_expect_tx(&in_full[s], bytes);
 #pragma unroll
@@ -131,6 +132,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
     for (int i = 0; i < my_tiles; ++i) {
       const int s = i % NST;
       mbar_wait(&in_full[s], (i / NST) & 1);
+      TSF_STAMP(p, C::W_CONV, 2 * i);
       uint8_t* tile = sIn + s * C::TILE_BYTES;
       constexpr int BATCH = 8;
       for (int u0 = (int)lane; u0 < units; u0 += 32 * BATCH) {
@@ -160,6 +162,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&in_conv[s]);
+      TSF_STAMP(p, C::W_CONV, 2 * i + 1);
     }
   } else if (warp == C::W_QK) {
     // ===================== QK^T issuer =====================
@@ -171,6 +174,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
         mbar_wait_sleep(&in_conv[s], (i / NST) & 1);
         // S[b] is free once the softmax of tile i - 2 has loaded it (and stored P)
         if (i >= 2) mbar_wait_sleep(&p_full[b], ((i - 2) >> 1) & 1);
+        TSF_STAMP(p, C::W_QK, i);
         tc_fence_after();
         const uint32_t xa = smem_u32(sIn + s * C::TILE_BYTES);
 #pragma unroll
@@ -193,6 +197,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
         mbar_wait_sleep(&p_full[b], (i >> 1) & 1);
         // O[b] is free once the epilogue of tile i - 2 has read it
         if (i >= 2) mbar_wait_sleep(&o_empty[b], ((i - 2) >> 1) & 1);
+        TSF_STAMP(p, C::W_PV, i);
         tc_fence_after();
         const uint32_t va = smem_u32(sIn + s * C::TILE_BYTES);
 #pragma unroll
@@ -226,6 +231,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
     for (int i = 0; i < my_tiles; ++i) {
       const int b = i & 1;
       mbar_wait(&s_full[b], (i >> 1) & 1);
+      TSF_STAMP(p, warp, 4 * i);
       tc_fence_after();
       uint32_t sv[WIN];
 #pragma unroll
@@ -252,10 +258,12 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
       }
       // P[b] and l[b] are free once the epilogue of tile i - 2 has read O[b] and
       // l[b] (which also means PV(i - 2) has consumed P[b])
+      TSF_STAMP(p, warp, 4 * i + 1);
       if (i >= 2) {
         mbar_wait(&o_empty[b], ((i - 2) >> 1) & 1);
         tc_fence_after();
       }
+      TSF_STAMP(p, warp, 4 * i + 2);
 #pragma unroll
       for (int c = 0; c < WIN / 2; c += 16)
         tmem_st_x16(tmem + lane_base + b * C::SLOT + C::COL_P + colstart / 2 + c, pk + c);
@@ -264,6 +272,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[b]);
+      TSF_STAMP(p, warp, 4 * i + 3);
     }
   } else {
     // ===================== epilogue (warps 4-7) =====================
@@ -280,6 +289,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
       mbar_wait(&o_full[b], (i >> 1) & 1);
       mbar_wait(&p_full[b], (i >> 1) & 1);               // l[b] written (release by the softmax warps)
       mbar_wait(&in_conv[s], (i / NST) & 1);             // residual rows converted (release by the converter)
+      TSF_STAMP(p, warp, 4 * i);
       tc_fence_after();
       float o[D];
 #pragma unroll
@@ -290,6 +300,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[b]);
+      TSF_STAMP(p, warp, 4 * i + 1);
       // staging tile i % 2 is free once the store of tile i - 2 has read it
       uint8_t* stg = sOut + b * C::TILE_BYTES;
       if (et == 0) bulk_wait_read1();
@@ -300,6 +311,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
         nf = epilogue_row_stage<D, 128, 128>(o, 1.0f / l, sIn + s * C::TILE_BYTES, r, stg, orow);
       }
       report_nonfinite(p, nf);
+      TSF_STAMP(p, warp, 4 * i + 2);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&in_empty[s]);        // the residual rows of this warp are read
@@ -318,6 +330,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
         }
         bulk_commit();
       }
+      TSF_STAMP(p, warp, 4 * i + 3);
     }
     if (et == 0) bulk_wait0();                           // every X_t store has landed
   }

@@ -384,9 +384,27 @@ static tsf_status dispatch_d(tsf_handle* h, bool packed, int win, int epi, cudaS
 
 // Attention over one view: q/k/v (q == k == v for the block stages).  The
 // output (o or y) uses the strides of `ov` (default: the input view's).
+// Joint attention with a block / causal mask (tsf_joint_attn): the flash kernel
+// with per-score masking (MASK = 1), default tile and exp settings.
+template <int D>
+static tsf_status launch_flash_masked(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
+                                      const CUtensorMap& mv, const AttnParams& p) {
+  constexpr int SUB = (D == 64) ? 96 : 128, EMU = (D == 64) ? 6 : 0;
+  constexpr int NST = (D == 128) ? 2 : 4;
+  using C = FlashCfg<D, EPI_OUT16, NST, SUB, 1>;
+  const long long items = (long long)p.n_qpairs * p.A * p.B;
+  if (items > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "too many work items");
+  AttnParams pp = p;
+  pp.num_items = (int)items;
+  pp.flags = 0;
+  const long long grid = items < h->num_sms ? items : h->num_sms;
+  return launch(h, attn_flash_kernel<D, EPI_OUT16, NST, EMU, SUB, 1, 1>, (int)grid, C::THREADS, C::SMEM, st, pp, mq,
+                mk, mv);
+}
+
 static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, const void* k, const void* vv, int epi,
                                 void* o, float* y, cudaStream_t st, const View* ov = nullptr,
-                                const DistOut* dist = nullptr) {
+                                const DistOut* dist = nullptr, int mask = 0) {
   if (!ov) ov = &v;
   h->use_pm = false;
   const int d = h->d;
@@ -418,7 +436,9 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
   p.trace = h->trace;
 #endif
   const bool f16 = (epi == EPI_BLOCK_S);  // X_t lives in fp16; x (BLOCK_T) arrives bf16
-  const bool packed = v.L <= 128;
+  const bool packed = v.L <= 128 && mask == 0;
+  p.mask_mode = mask;
+  p.mask_n = h->N;
   int win = 128;
   CUtensorMap mq, mk, mv, mo;
   memset(&mo, 0, sizeof mo);
@@ -461,6 +481,13 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
     if ((s = make_map(h, &mq, q, d, v, 128, 1, 1, f16)) != TSF_OK) return s;
     if ((s = make_map(h, &mk, k, d, v, sub, 1, 1, f16)) != TSF_OK) return s;
     if ((s = make_map(h, &mv, vv, d, v, sub, 1, 1, f16)) != TSF_OK) return s;
+    if (mask) {
+      switch (d) {
+        case 32: return launch_flash_masked<32>(h, st, mq, mk, mv, p);
+        case 64: return launch_flash_masked<64>(h, st, mq, mk, mv, p);
+        default: return launch_flash_masked<128>(h, st, mq, mk, mv, p);
+      }
+    }
   }
   switch (d) {
     case 32: return dispatch_d<32>(h, packed, win, epi, st, mq, mk, mv, mo, p);
@@ -804,6 +831,25 @@ tsf_status tsf_spatial_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k,
   cudaStream_t st = (cudaStream_t)stream;
   StageTimer tm(h, st, 1);
   s = run_attention(h, spatial_view(Kl, h->N, h->H, h->d), q, k, v, EPI_OUT16, o, nullptr, st);
+  tm.done();
+  return s;
+}
+
+tsf_status tsf_joint_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v, tsf_bf16* o,
+                          int mask, void* stream) {
+  if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
+  h->launches = 0;
+  if (mask < TSF_MASK_NONE || mask > TSF_MASK_CAUSAL_FRAMES) return fail(h, TSF_ERR_CONFIG, "unknown mask");
+  if (h->world != 1) return fail(h, TSF_ERR_UNSUPPORTED, "joint attention runs on single-GPU handles");
+  if ((long long)h->K * h->N > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "K * N too large");
+  const size_t bytes = (size_t)h->K * h->N * h->H * h->d * 2;
+  tsf_status s = check_ptrs(h, {q, k, v}, o, bytes, bytes);
+  if (s != TSF_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  // all K*N tokens as one sequence per head: [K, N, H, d] = [1, K*N, H, d]
+  const View jv{h->K * h->N, h->H, 1, (long long)h->H * h->d, (long long)h->d, (long long)h->K * h->N * h->H * h->d};
+  StageTimer tm(h, st, 5);
+  s = run_attention(h, jv, q, k, v, EPI_OUT16, o, nullptr, st, nullptr, nullptr, mask);
   tm.done();
   return s;
 }

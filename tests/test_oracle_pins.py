@@ -68,12 +68,67 @@ def test_joint_unmasked_matches_brute_force_loops():
     np.testing.assert_allclose(oracle.joint_masked(q, k, v), out, rtol=0, atol=1e-12)
 
 
+def test_joint_causal_frames_matches_brute_force_loops():
+    """Causal-in-time joint attention (SURVEY NEXT-4 variant): token (t, n) attends
+    to every (t', n') with t' <= t; tiny brute force with math.exp loops."""
+    K, N, H, d = 3, 2, 2, 3
+    q, k, v = rand(K, N, H, d), rand(K, N, H, d), rand(K, N, H, d)
+    out = np.zeros_like(q)
+    for h in range(H):
+        for t in range(K):
+            for n in range(N):
+                keys = [(a, b) for a in range(t + 1) for b in range(N)]
+                w = [math.exp(sum(q[t, n, h, i] * k[a, b, h, i] for i in range(d)) / math.sqrt(d)) for a, b in keys]
+                z = sum(w)
+                for i in range(d):
+                    out[t, n, h, i] = sum(wj * v[a, b, h, i] for wj, (a, b) in zip(w, keys)) / z
+    np.testing.assert_allclose(oracle.joint_masked(q, k, v, oracle.mask_causal_frames(K, N)), out,
+                               rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("shape", [(3, 5, 2, 4), (1, 7, 1, 8), (4, 1, 2, 2)])
+def test_joint_causal_frames_special_cases(shape):
+    """Frame 0 attends only to itself (= spatial attention of frame 0); the last
+    frame attends to everything (= unmasked joint attention); K = 1 is spatial."""
+    q, k, v = rand(*shape), rand(*shape), rand(*shape)
+    K, N = shape[:2]
+    c = oracle.joint_masked(q, k, v, oracle.mask_causal_frames(K, N))
+    np.testing.assert_allclose(c[0], oracle.spatial(q, k, v)[0], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(c[K - 1], oracle.joint_masked(q, k, v)[K - 1], rtol=0, atol=1e-12)
+    m = oracle.mask_causal_frames(K, N)
+    assert m.sum() == N * N * K * (K + 1) // 2                 # lower block triangle incl. diagonal
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_joint_rows_match_full_joint(causal):
+    K, N, H, d = 3, 4, 2, 4
+    q, k, v = rand(K, N, H, d), rand(K, N, H, d), rand(K, N, H, d)
+    full = oracle.joint_masked(q, k, v, oracle.mask_causal_frames(K, N) if causal else None)
+    rows = [(0, 0, 0), (2, 3, 1), (1, 2, 0), (2, 0, 1)]
+    got = oracle.joint_rows(q, k, v, rows, causal_frames=causal)
+    np.testing.assert_allclose(got, np.array([full[t, n, h] for t, n, h in rows]), rtol=0, atol=1e-12)
+
+
 # --- library routine: torch SDPA in fp64 on CPU -----------------------------
 
 def sdpa(q, k, v):
     """[G, L, d] fp64 through torch.nn.functional.scaled_dot_product_attention."""
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a))[None]
     return torch.nn.functional.scaled_dot_product_attention(t(q), t(k), t(v))[0].numpy()
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_joint_matches_library_sdpa(causal):
+    """Unmasked global attention over all K*N tokens and its
+    causal-frame variant = torch SDPA fp64 (boolean attn_mask)."""
+    K, N, H, d = 3, 5, 2, 8
+    q, k, v = rand(K, N, H, d), rand(K, N, H, d), rand(K, N, H, d)
+    g = lambda a: torch.from_numpy(np.ascontiguousarray(a.reshape(K * N, H, d).transpose(1, 0, 2)))
+    m = torch.from_numpy(oracle.mask_causal_frames(K, N)) if causal else None
+    ref = torch.nn.functional.scaled_dot_product_attention(g(q), g(k), g(v), attn_mask=m).numpy()
+    ref = ref.transpose(1, 0, 2).reshape(K, N, H, d)
+    got = oracle.joint_masked(q, k, v, oracle.mask_causal_frames(K, N) if causal else None)
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-12)
 
 
 @pytest.mark.parametrize("shape", [(6, 7, 3, 16), (1, 33, 2, 32), (9, 1, 2, 64)])
@@ -196,9 +251,11 @@ def test_I6_linear_in_v_and_convex():
 
 def test_I7_large_logit_selects_argmax():
     K, N, H, d = 1, 7, 1, 4
-    k = rand(K, N, H, d)
-    v = rand(K, N, H, d)
-    q = np.broadcast_to(k[:, 3:4], k.shape) * 1e3       # argmax key is n=3 for every query
+    g = np.random.default_rng(7)                          # own stream: independent of test order
+    k = g.normal(size=(K, N, H, d))
+    k /= np.linalg.norm(k, axis=-1, keepdims=True)        # unit keys: q = 1e3 k_3 has a unique argmax n = 3
+    v = g.normal(size=(K, N, H, d))
+    q = np.broadcast_to(k[:, 3:4], k.shape) * 1e3
     o = oracle.spatial(q, k, v)
     np.testing.assert_allclose(o, np.broadcast_to(v[:, 3:4], v.shape), atol=1e-9, rtol=0)
 
