@@ -95,6 +95,22 @@ tsf_status tsf_spatial_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k,
 tsf_status tsf_joint_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v, tsf_bf16* o,
                           int mask, void* stream);
 
+/* STORM per-layer attention (sec. IV-B):
+ * spatial self-attention on the current state plus cross-attention to M
+ * compressed history tokens, mixed by the noise gate g(sigma), identity
+ * projections (reading G1):
+ *   y[b] = u[b] + (1 - g) S(u[b], u[b], u[b]) + g C(u[b], ctx[b], ctx[b]),
+ *   g = sigma^2 / (sigma^2 + sigma_data^2)   (reading G18),
+ * S = softmax attention over the N tokens of u[b] (per head), C = attention of
+ * those N queries over the M context tokens of ctx[b] (per head), scale
+ * 1/sqrt(d).  The handle's K is the number B of independent states.
+ * u: bf16 [K, N, H, d]; ctx: bf16 [K, M, H, d], M >= 1; y: fp32 [K, N, H, d].
+ * bf16 operands and P, fp32 accumulation; y must not overlap u or ctx.
+ * sigma >= 0 and finite, sigma_data > 0 (else TSF_ERR_CONFIG).  Two launches
+ * (cross writes y, self adds into it).  Single-GPU handles only. */
+tsf_status tsf_storm_attn(tsf_handle* h, const tsf_bf16* u, const tsf_bf16* ctx, int M, double sigma,
+                          double sigma_data, float* y, void* stream);
+
 /* Divided space-time block, temporal then spatial ("followed by"), with
  * identity projections and residual weight 1 (readings G1, G5):
  *   X_t = x + T(x, x, x);   y = X_t + S(X_t, X_t, X_t).
@@ -198,7 +214,7 @@ int tsf_world_size(const tsf_handle* h);
  * returns the summed milliseconds and the number of recorded launches of
  * stage 0 = temporal attention, 1 = spatial attention, 2 = reshard
  * (all-to-all + unpack), 3 = host<->device copies, 4 = tsf_transpose,
- * 5 = tsf_joint_attn. */
+ * 5 = tsf_joint_attn, 6 = tsf_storm_attn. */
 tsf_status tsf_set_timing(tsf_handle* h, int enable);
 tsf_status tsf_stage_ms(tsf_handle* h, int stage, float* total_ms, int* n_records);
 

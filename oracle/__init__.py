@@ -29,6 +29,9 @@ from .attention import (  # noqa: F401
     mask_spatial,
     mask_causal_frames,
     joint_rows,
+    noise_gate,
+    cross,
+    storm_attention,
     temporal_rows,
     spatial_rows,
     block_rows,

@@ -177,6 +177,64 @@ def joint_rows(q, k, v, rows: Iterable[Sequence[int]], causal_frames: bool = Fal
 
 
 # ---------------------------------------------------------------------------
+# STORM per-layer attention: spatial self-attention on the
+# current state plus cross-attention to M compressed history tokens, mixed by
+# the noise gate (section IV-B)
+# ---------------------------------------------------------------------------
+
+def noise_gate(sigma: float, sigma_data: float) -> float:
+    """g(sigma) = sigma^2 / (sigma^2 + sigma_data^2).
+
+    P:379 fixes only the behaviour ("at high noise levels, STORM relies more on
+    historical input and temporal cross-attention, while at low noise levels,
+    it emphasizes ... spatial self-attention"); the rational form is SPEC.md's
+    reading (examples g(0) = 0, g(sigma_data) = 0.5,
+    g(3 sigma_data) = 0.9), reading G18.
+    """
+    if not sigma_data > 0:
+        raise ValueError("sigma_data must be > 0")
+    if sigma < 0:
+        raise ValueError("sigma must be >= 0")
+    return sigma * sigma / (sigma * sigma + sigma_data * sigma_data)
+
+
+def cross(q: np.ndarray, kv_k: np.ndarray, kv_v: np.ndarray) -> np.ndarray:
+    """Cross-attention of the N query tokens of each (frame, head) over the M
+    context tokens of the same (frame, head): q [B, N, H, d], k/v [B, M, H, d]."""
+    _check(q, kv_k, kv_v)
+    B, N, H, d = q.shape
+    M = kv_k.shape[1]
+    g = lambda a, L: a.transpose(0, 2, 1, 3).reshape(B * H, L, d)
+    o = _grouped_qk(g(q, N), g(kv_k, M), g(kv_v, M))
+    return o.reshape(B, H, N, d).transpose(0, 2, 1, 3).copy()
+
+
+def _grouped_qk(Qg: np.ndarray, Kg: np.ndarray, Vg: np.ndarray) -> np.ndarray:
+    """attend() per group with query and key lengths that may differ."""
+    G, Lq, d = Qg.shape
+    Lk = Kg.shape[1]
+    step = max(1, _CHUNK_BYTES // max(1, Lq * Lk * 8 * 3))
+    out = np.empty((G, Lq, d))
+    for g0 in range(0, G, step):
+        out[g0:g0 + step] = attend(Qg[g0:g0 + step], Kg[g0:g0 + step], Vg[g0:g0 + step])
+    return out
+
+
+def storm_attention(u: np.ndarray, ctx: np.ndarray, sigma: float, sigma_data: float) -> np.ndarray:
+    """One STORM layer's attention with identity projections (reading G1):
+
+        y = u + (1 - g) SelfAttn_spatial(u) + g CrossAttn(u, ctx),  g = noise_gate(sigma)
+
+    u: [B, N, H, d] current-state tokens (B independent states), ctx:
+    [B, M, H, d] compressed temporal representation ("cross-attention
+    between the current state and the compressed temporal representation";
+    per-layer update form from SPEC.md S:246).
+    """
+    g = noise_gate(sigma, sigma_data)
+    return u + (1.0 - g) * spatial(u, u, u) + g * cross(u, ctx, ctx)
+
+
+# ---------------------------------------------------------------------------
 # sampled rows (any size): an output row depends on its query row and its group
 # ---------------------------------------------------------------------------
 

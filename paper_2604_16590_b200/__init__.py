@@ -30,7 +30,8 @@ STATUS_NAMES = {0: "TSF_OK", 2: "TSF_ERR_CONFIG", 3: "TSF_ERR_NUMERIC", 4: "TSF_
                 5: "TSF_ERR_CUDA", 6: "TSF_ERR_NCCL", 7: "TSF_ERR_NOMEM"}
 TSF_T2S, TSF_S2T = 0, 1
 TSF_MASK_NONE, TSF_MASK_TEMPORAL, TSF_MASK_SPATIAL, TSF_MASK_CAUSAL_FRAMES = 0, 1, 2, 3
-STAGE_TEMPORAL, STAGE_SPATIAL, STAGE_RESHARD, STAGE_COPY, STAGE_TRANSPOSE, STAGE_JOINT = 0, 1, 2, 3, 4, 5
+STAGE_TEMPORAL, STAGE_SPATIAL, STAGE_RESHARD, STAGE_COPY, STAGE_TRANSPOSE, STAGE_JOINT, STAGE_STORM = \
+    0, 1, 2, 3, 4, 5, 6
 
 # Every function declared in include/tsf.h: (name, restype, argtypes)
 _P, _I, _F = ctypes.c_void_p, ctypes.c_int, ctypes.c_float
@@ -39,6 +40,7 @@ SIGNATURES = [
     ("tsf_temporal_attn", _I, [_P, _P, _P, _P, _P, _P]),
     ("tsf_spatial_attn", _I, [_P, _P, _P, _P, _P, _P]),
     ("tsf_joint_attn", _I, [_P, _P, _P, _P, _P, _I, _P]),
+    ("tsf_storm_attn", _I, [_P, _P, _P, _I, ctypes.c_double, ctypes.c_double, _P, _P]),
     ("tsf_spacetime_block", _I, [_P, _P, _P, _P]),
     ("tsf_spacetime_block_host", _I, [_P, _P, _P, _P]),
     ("tsf_destroy", None, [_P]),
@@ -204,6 +206,21 @@ class Layer:
         _need(out, torch.bfloat16, shp, "out")
         _check(lib().tsf_joint_attn(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), int(mask),
                                     _stream_ptr(stream)), self._h)
+        return out
+
+    def storm(self, u, ctx, sigma: float, sigma_data: float, out=None, stream=None):
+        """tsf_storm_attn: y = u + (1-g) SelfAttn(u) + g CrossAttn(u, ctx), g = s^2/(s^2 + s_data^2).
+        u bf16 [K, N, H, d] (K independent states), ctx bf16 [K, M, H, d] -> y fp32 [K, N, H, d]."""
+        import torch
+        _need(u, torch.bfloat16, (self.K, self.N, self.H, self.d), "u")
+        if ctx.dim() != 4 or tuple(ctx.shape[::2]) != (self.K, self.H) or ctx.shape[3] != self.d:
+            raise ValueError(f"ctx must have shape ({self.K}, M, {self.H}, {self.d}), got {tuple(ctx.shape)}")
+        _need(ctx, torch.bfloat16, tuple(ctx.shape), "ctx")
+        out = torch.empty((self.K, self.N, self.H, self.d), dtype=torch.float32, device=u.device) \
+            if out is None else out
+        _need(out, torch.float32, (self.K, self.N, self.H, self.d), "out")
+        _check(lib().tsf_storm_attn(self._h, u.data_ptr(), ctx.data_ptr(), int(ctx.shape[1]), float(sigma),
+                                    float(sigma_data), out.data_ptr(), _stream_ptr(stream)), self._h)
         return out
 
     def block(self, x, out=None, stream=None):

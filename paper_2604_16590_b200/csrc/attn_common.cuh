@@ -31,11 +31,13 @@ enum EpiMode : int {
   EPI_BLOCK_T = 1,  // X_t = x + O/l -> fp16 X_t       (block, temporal stage): x arrives bf16 and
                     //   is converted to fp16 in shared memory; fp16 operands, fp16 P
   EPI_BLOCK_S = 2,  // y = X_t + O/l -> fp32 y         (block, spatial stage), fp16 operands, fp16 P
+  EPI_STORM_X = 3,  // y = u + g O/l -> fp32 y         (STORM cross-attention, q = u, k = v = ctx), bf16
+  EPI_STORM_S = 4,  // y += (1 - g) O/l (fp32 y)       (STORM self-attention, q = k = v = u), bf16
 };
 template <int EPI> struct EpiTraits {
-  static constexpr bool F16 = (EPI != EPI_OUT16);       // MMA operand / P type is fp16 (else bf16)
+  static constexpr bool F16 = (EPI == EPI_BLOCK_T || EPI == EPI_BLOCK_S);  // MMA operand / P type fp16 (else bf16)
   static constexpr bool CONVERT = (EPI == EPI_BLOCK_T);  // tiles land as bf16, converted in smem
-  static constexpr bool SHARED = (EPI != EPI_OUT16);     // q = k = v: one tile serves Q, K and V
+  static constexpr bool SHARED = (EPI == EPI_BLOCK_T || EPI == EPI_BLOCK_S || EPI == EPI_STORM_S);  // q = k = v
 };
 
 // In-place bf16 -> fp16 conversion of one 16-byte unit (8 elements).  Exact
@@ -86,6 +88,10 @@ struct AttnParams {
   // mask_mode 1 = temporal block mask [n' = n], 2 = spatial block mask
   // [t' = t], 3 = causal frames [t' <= t]; mask_n = N tokens per frame
   int mask_mode, mask_n;
+  // key/value sequence length (= L except for cross-attention, EPI_STORM_X)
+  int Lk;
+  // STORM epilogue weight: g for EPI_STORM_X, 1 - g for EPI_STORM_S
+  float gate;
 };
 constexpr int FLASH_PINGPONG = 2;
 constexpr int FLASH_RES_GLOBAL = 4;  // flash kernel: block residual from global memory, not the Q tile (diagnostics)
@@ -185,11 +191,26 @@ __device__ __forceinline__ uint32_t epilogue_row(const AttnParams& p, const floa
       w.z = pack2<false>(v[4], v[5]);
       w.w = pack2<false>(v[6], v[7]);
       *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o) + off + 8 * u) = w;
+    } else if constexpr (EPI == EPI_STORM_S) {  // y += (1 - g) O/l
+      float4* yp = reinterpret_cast<float4*>(p.y + off + 8 * u);
+      float4 y0 = yp[0], y1 = yp[1];
+      const float w = p.gate;
+      y0.x = fmaf(w, v[0], y0.x); y0.y = fmaf(w, v[1], y0.y); y0.z = fmaf(w, v[2], y0.z); y0.w = fmaf(w, v[3], y0.w);
+      y1.x = fmaf(w, v[4], y1.x); y1.y = fmaf(w, v[5], y1.y); y1.z = fmaf(w, v[6], y1.z); y1.w = fmaf(w, v[7], y1.w);
+      yp[0] = y0;
+      yp[1] = y1;
     } else {
       const uint4 rr = tile_row_u4<D, ROWS>(res_tile, r, u0 + u);
       const float2 x0 = unpack2<F16>(rr.x), x1 = unpack2<F16>(rr.y), x2 = unpack2<F16>(rr.z),
                    x3 = unpack2<F16>(rr.w);
-      if constexpr (EPI == EPI_BLOCK_S) {
+      if constexpr (EPI == EPI_STORM_X) {  // y = u + g O/l
+        const float w = p.gate;
+        float4 y0, y1;
+        y0.x = fmaf(w, v[0], x0.x); y0.y = fmaf(w, v[1], x0.y); y0.z = fmaf(w, v[2], x1.x); y0.w = fmaf(w, v[3], x1.y);
+        y1.x = fmaf(w, v[4], x2.x); y1.y = fmaf(w, v[5], x2.y); y1.z = fmaf(w, v[6], x3.x); y1.w = fmaf(w, v[7], x3.y);
+        *reinterpret_cast<float4*>(p.y + off + 8 * u) = y0;
+        *reinterpret_cast<float4*>(p.y + off + 8 * u + 4) = y1;
+      } else if constexpr (EPI == EPI_BLOCK_S) {
         float4 y0, y1;
         y0.x = x0.x + v[0]; y0.y = x0.y + v[1]; y0.z = x1.x + v[2]; y0.w = x1.y + v[3];
         y1.x = x2.x + v[4]; y1.y = x2.y + v[5]; y1.z = x3.x + v[6]; y1.w = x3.y + v[7];
@@ -230,12 +251,27 @@ __device__ __forceinline__ uint32_t epilogue_row_g(const AttnParams& p, const fl
       w.z = pack2<false>(v[4], v[5]);
       w.w = pack2<false>(v[6], v[7]);
       *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o) + off + 8 * u) = w;
+    } else if constexpr (EPI == EPI_STORM_S) {  // y += (1 - g) O/l
+      float4* yp = reinterpret_cast<float4*>(p.y + off + 8 * u);
+      float4 y0 = yp[0], y1 = yp[1];
+      const float w = p.gate;
+      y0.x = fmaf(w, v[0], y0.x); y0.y = fmaf(w, v[1], y0.y); y0.z = fmaf(w, v[2], y0.z); y0.w = fmaf(w, v[3], y0.w);
+      y1.x = fmaf(w, v[4], y1.x); y1.y = fmaf(w, v[5], y1.y); y1.z = fmaf(w, v[6], y1.z); y1.w = fmaf(w, v[7], y1.w);
+      yp[0] = y0;
+      yp[1] = y1;
     } else {
       constexpr bool RES_F16 = (EPI == EPI_BLOCK_S);
       const uint4 rr = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(p.res) + in_off + 8 * u);
       const float2 x0 = unpack2<RES_F16>(rr.x), x1 = unpack2<RES_F16>(rr.y), x2 = unpack2<RES_F16>(rr.z),
                    x3 = unpack2<RES_F16>(rr.w);
-      if constexpr (EPI == EPI_BLOCK_S) {
+      if constexpr (EPI == EPI_STORM_X) {  // y = u + g O/l
+        const float w = p.gate;
+        float4 y0, y1;
+        y0.x = fmaf(w, v[0], x0.x); y0.y = fmaf(w, v[1], x0.y); y0.z = fmaf(w, v[2], x1.x); y0.w = fmaf(w, v[3], x1.y);
+        y1.x = fmaf(w, v[4], x2.x); y1.y = fmaf(w, v[5], x2.y); y1.z = fmaf(w, v[6], x3.x); y1.w = fmaf(w, v[7], x3.y);
+        *reinterpret_cast<float4*>(p.y + off + 8 * u) = y0;
+        *reinterpret_cast<float4*>(p.y + off + 8 * u + 4) = y1;
+      } else if constexpr (EPI == EPI_BLOCK_S) {
         float4 y0, y1;
         y0.x = x0.x + v[0]; y0.y = x0.y + v[1]; y0.z = x1.x + v[2]; y0.w = x1.y + v[3];
         y1.x = x2.x + v[4]; y1.y = x2.y + v[5]; y1.z = x3.x + v[6]; y1.w = x3.y + v[7];

@@ -408,9 +408,9 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         const uint32_t tSb = tSrow + SUB * b;
         const uint32_t tPb = C::SEP ? tmem + lane_base + C::COL_P + (SUB / 2) * t + hf * (CW / 2)
                                     : tSb + SUB / 2;
-        TSF_STAMP(p, warp, 6 * i + 0);
+        TSF_STAMP(p, warp, 7 * i + 0);
         mbar_wait(&s_full[b], sphase);
-        TSF_STAMP(p, warp, 6 * i + 1);
+        TSF_STAMP(p, warp, 7 * i + 1);
         tc_fence_after();
         uint32_t sv[CW];
 #pragma unroll
@@ -424,8 +424,8 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           __syncwarp();
           if (lane == 0) mbar_arrive(&s_free[t]);
         }
-        TSF_STAMP(p, warp, 6 * i + 2);
-        const int valid = L - i * SUB - hf * CW;  // columns >= valid are beyond the sequence
+        TSF_STAMP(p, warp, 7 * i + 2);
+        const int valid = p.Lk - i * SUB - hf * CW;  // columns >= valid are beyond the key sequence
         if (valid < CW) {
 #pragma unroll
           for (int c = 0; c < CW; ++c) sv[c] = (c < valid) ? sv[c] : 0xFF800000u;  // -inf
@@ -490,7 +490,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           }
         }
         const float m_new = fmaxf(m_run, mx * sl2);
-        TSF_STAMP(p, warp, 6 * i + 3);
+        TSF_STAMP(p, warp, 7 * i + 3);
         // Move the max for the whole warp (exact for every row) when some row's
         // max grew by more than RESCALE_LOG2; O_t (and its l columns) is
         // rescaled by alpha before P_t is stored, once PV_t(G-1) has retired.
@@ -574,22 +574,27 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
             else tmem_st_x8(tPb + c0 / 2, pk);
           }
         }
+        TSF_STAMP(p, warp, 7 * i + 4);
         if constexpr (C::SEP) {
+          // ping-pong: hand the MUFU to the other tile's warps as soon as the
+          // exponentials are done, before waiting for PV_t(G-1) and storing P
+          if (pingpong) named_bar_arrive(2 - t, 256 * SPLIT);
           before_p_store();
 #pragma unroll
           for (int c0 = 0; c0 < CW; c0 += PW) {
             if constexpr (PW == 32) tmem_st_x16(tPb + c0 / 2, pk_all + c0 / 2);
             else tmem_st_x8(tPb + c0 / 2, pk_all + c0 / 2);
           }
+        } else {
+          if (pingpong) named_bar_arrive(2 - t, 256 * SPLIT);
         }
-        if (pingpong) named_bar_arrive(2 - t, 256 * SPLIT);
         l_run += ls0 + ls1;
-        TSF_STAMP(p, warp, 6 * i + 4);
+        TSF_STAMP(p, warp, 7 * i + 5);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[C::SEP ? t : b]);
-        TSF_STAMP(p, warp, 6 * i + 5);
+        TSF_STAMP(p, warp, 7 * i + 6);
       }
 
       // ---- epilogue of item k: this warp's OCOLS columns of its rows ----

@@ -7,16 +7,22 @@
 // byte of X_t written once, so the kernel is organised as a stream in which
 // every role works on a different tile at the same time:
 //
-//   warp  8      TMA producer: x tiles into an NST-deep input ring
-//   warp 11      converter: bf16 -> fp16 in place (the MMA operands and the
-//                residual are fp16, reading G8)
-//   warp  9      QK^T issuer: S[b] = X X^T of tile i into TMEM slot b = i % 2
+//   warp 16      TMA producer: x tiles into an NST-deep input ring
+//   warps 12-15  converters: bf16 -> fp16 in place (the MMA operands and the
+//                residual are fp16, reading G8); tile i by warp 12 + i % 4
+//   warp 17      QK^T issuer: S[b] = X X^T of tile i into TMEM slot b = i % 2
 //   warps 0-3    softmax: block-diagonal window softmax of S[b] -> P[b] (TMEM),
 //                row sums l of the rounded P -> shared memory
-//   warp 10      PV issuer: O[b] = P[b] X
-//   warps 4-7    epilogue: X_t = x + O[b] / l into an fp16 staging tile
-//                (regrouped by destination rank when distributed), one TMA
-//                store per tile (per destination), input stage released
+//   warp 18      PV issuer: O[b] = P[b] X
+//   warps 4-7,   epilogue warpgroup b (slot b's tiles): X_t = x + O[b] / l into
+//   8-11         an fp16 staging tile (regrouped by destination rank when
+//                distributed), one TMA store per tile (per destination),
+//                input stage released
+//
+// Measured on B200 (tools/trace_stream.py): converting one 16 KB tile costs a
+// warp ~2300 cycles and the epilogue of one tile ~1700, against a ~1400-cycle
+// per-tile budget at the HBM roofline, hence four converters and two
+// epilogue warpgroups.
 //
 // A 128-row tile holds G = Ab * Bb whole groups of L = K rows (group-major,
 // see attn_common.cuh); one 128x128 QK^T and one 128xD PV MMA cover all of
@@ -47,19 +53,20 @@ struct StreamCfg {
   static constexpr int LBUF_BYTES = 2 * 128 * 4;              // l per row per slot
   static constexpr int BAR_BYTES = 512;
   static constexpr int SMEM = NST * TILE_BYTES + 2 * TILE_BYTES + LBUF_BYTES + BAR_BYTES + 1024;
-  static constexpr int THREADS = 384;
-  static constexpr int W_EPI = 4, W_TMA = 8, W_QK = 9, W_PV = 10, W_CONV = 11;
+  static constexpr int THREADS = 640;
+  static constexpr int W_EPI = 4, W_CONV = 12, NCONV = 4, W_TMA = 16, W_QK = 17, W_PV = 18;
 };
 
-template <int D, int WIN, int NST>
-__global__ void __launch_bounds__(384, 1)
+template <int D, int WIN, int NST, int LT>
+__global__ void __launch_bounds__(640, 1)
 attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap to,
                    const __grid_constant__ PeerMaps pm, const AttnParams p) {
   using C = StreamCfg<D, WIN, NST>;
+  static_assert(LT == 0 || (WIN == 32 && 32 % LT == 0 && LT >= 2), "compact softmax: L divides 32");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sIn = smem;                                   // NST input tiles (x, bf16 -> fp16 in place)
-  uint8_t* sOut = smem + NST * C::TILE_BYTES;            // 2 fp16 X_t staging tiles
+  uint8_t* sOut = smem + NST * C::TILE_BYTES;            // fp16 X_t staging tile of each epilogue warpgroup
   float* lbuf = reinterpret_cast<float*>(sOut + 2 * C::TILE_BYTES);   // [2][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + 2 * C::TILE_BYTES + C::LBUF_BYTES);
   uint64_t* in_full = bars;              // [NST] TMA
@@ -115,7 +122,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
         const int tile = blockIdx.x + i * gridDim.x;
         const int s = i % NST;
         if (i >= NST) mbar_wait_sleep(&in_empty[s], ((i / NST) - 1) & 1);
-        TSF_STAMP(p, C::W_TMA, i);
+        TSF_STAMP(p, 12 + (C::W_TMA), i);
         const int a0 = (tile % p.tiles_a) * p.Ab, b0 = (tile / p.tiles_a) * p.Bb;
         mbar_arrive_expect_tx(&in_full[s], bytes);
 #pragma unroll
@@ -124,15 +131,15 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
       }
     }
     __syncwarp();
-  } else if (warp == C::W_CONV) {
-    // ===================== converter: bf16 -> fp16 in place =====================
+  } else if (warp >= C::W_CONV && warp < C::W_CONV + C::NCONV) {
+    // ===================== converters: bf16 -> fp16 in place =====================
     constexpr int UPR = D / 8;                 // 16-byte units per row
     constexpr int UPC = C::SWB / 16;           // units per chunk row
     const int units = rows_used * UPR;         // rows are whole units: the swizzle does not matter
-    for (int i = 0; i < my_tiles; ++i) {
+    for (int i = (int)(warp - C::W_CONV); i < my_tiles; i += C::NCONV) {
       const int s = i % NST;
       mbar_wait(&in_full[s], (i / NST) & 1);
-      TSF_STAMP(p, C::W_CONV, 2 * i);
+      TSF_STAMP(p, 12 + (warp), 2 * (i / C::NCONV));
       uint8_t* tile = sIn + s * C::TILE_BYTES;
       constexpr int BATCH = 8;
       for (int u0 = (int)lane; u0 < units; u0 += 32 * BATCH) {
@@ -162,7 +169,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&in_conv[s]);
-      TSF_STAMP(p, C::W_CONV, 2 * i + 1);
+      TSF_STAMP(p, 12 + (warp), 2 * (i / C::NCONV) + 1);
     }
   } else if (warp == C::W_QK) {
     // ===================== QK^T issuer =====================
@@ -174,7 +181,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
         mbar_wait_sleep(&in_conv[s], (i / NST) & 1);
         // S[b] is free once the softmax of tile i - 2 has loaded it (and stored P)
         if (i >= 2) mbar_wait_sleep(&p_full[b], ((i - 2) >> 1) & 1);
-        TSF_STAMP(p, C::W_QK, i);
+        TSF_STAMP(p, 12 + (C::W_QK), i);
         tc_fence_after();
         const uint32_t xa = smem_u32(sIn + s * C::TILE_BYTES);
 #pragma unroll
@@ -197,7 +204,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
         mbar_wait_sleep(&p_full[b], (i >> 1) & 1);
         // O[b] is free once the epilogue of tile i - 2 has read it
         if (i >= 2) mbar_wait_sleep(&o_empty[b], ((i - 2) >> 1) & 1);
-        TSF_STAMP(p, C::W_PV, i);
+        TSF_STAMP(p, 12 + (C::W_PV), i);
         tc_fence_after();
         const uint32_t va = smem_u32(sIn + s * C::TILE_BYTES);
 #pragma unroll
@@ -231,39 +238,68 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
     for (int i = 0; i < my_tiles; ++i) {
       const int b = i & 1;
       mbar_wait(&s_full[b], (i >> 1) & 1);
-      TSF_STAMP(p, warp, 4 * i);
+      TSF_STAMP(p, 12 + (warp), 4 * i);
       tc_fence_after();
       uint32_t sv[WIN];
 #pragma unroll
       for (int c = 0; c < WIN; c += 32) tmem_ld_x32(tmem + lane_base + b * C::SLOT + C::COL_S + colstart + c, sv + c);
       tmem_wait_ld();
-      float m = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < WIN; ++c) {
-        const bool ok = row_ok && c >= lo && c < hi;
-        m = ok ? fmaxf(m, __uint_as_float(sv[c])) : m;
-      }
-      const float mb = (m == -INFINITY) ? 0.f : m * sl2;
       float l = 0.f;
       uint32_t pk[WIN / 2];
+      if constexpr (LT > 0) {
+        // compact path (L = LT divides 32): the row's LT valid scores are the
+        // LT-column block number gsel of its 32-column window; only those are
+        // exponentiated (LT instead of 32 exps per row)
+        const int gsel = (int)lane / LT;
+        float v[LT];
 #pragma unroll
-      for (int c = 0; c < WIN; c += 2) {
-        const bool ok0 = row_ok && c >= lo && c < hi;
-        const bool ok1 = row_ok && c + 1 >= lo && c + 1 < hi;
-        const float p0 = ok0 ? ex2(fmaf(__uint_as_float(sv[c]), sl2, -mb)) : 0.f;
-        const float p1 = ok1 ? ex2(fmaf(__uint_as_float(sv[c + 1]), sl2, -mb)) : 0.f;
-        pk[c / 2] = pack2<true>(p0, p1);
-        const float2 pr = unpack2<true>(pk[c / 2]);
-        l += pr.x + pr.y;                                // l sums the rounded P (reading G9)
+        for (int k = 0; k < LT; ++k) {
+          uint32_t x = sv[k];
+#pragma unroll
+          for (int g2 = 1; g2 < 32 / LT; ++g2) x = (gsel == g2) ? sv[g2 * LT + k] : x;
+          v[k] = __uint_as_float(x);
+        }
+        float m = v[0];
+#pragma unroll
+        for (int k = 1; k < LT; ++k) m = fmaxf(m, v[k]);
+        const float mb = m * sl2;
+        uint32_t pw[LT / 2];
+#pragma unroll
+        for (int k = 0; k < LT; k += 2) {
+          pw[k / 2] = pack2<true>(ex2(fmaf(v[k], sl2, -mb)), ex2(fmaf(v[k + 1], sl2, -mb)));
+          const float2 pr = unpack2<true>(pw[k / 2]);
+          l += pr.x + pr.y;                              // l sums the rounded P (reading G9)
+        }
+#pragma unroll
+        for (int c = 0; c < WIN / 2; ++c)
+          pk[c] = (row_ok && c / (LT / 2) == gsel) ? pw[c % (LT / 2)] : 0u;
+      } else {
+        float m = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < WIN; ++c) {
+          const bool ok = row_ok && c >= lo && c < hi;
+          m = ok ? fmaxf(m, __uint_as_float(sv[c])) : m;
+        }
+        const float mb = (m == -INFINITY) ? 0.f : m * sl2;
+#pragma unroll
+        for (int c = 0; c < WIN; c += 2) {
+          const bool ok0 = row_ok && c >= lo && c < hi;
+          const bool ok1 = row_ok && c + 1 >= lo && c + 1 < hi;
+          const float p0 = ok0 ? ex2(fmaf(__uint_as_float(sv[c]), sl2, -mb)) : 0.f;
+          const float p1 = ok1 ? ex2(fmaf(__uint_as_float(sv[c + 1]), sl2, -mb)) : 0.f;
+          pk[c / 2] = pack2<true>(p0, p1);
+          const float2 pr = unpack2<true>(pk[c / 2]);
+          l += pr.x + pr.y;                              // l sums the rounded P (reading G9)
+        }
       }
       // P[b] and l[b] are free once the epilogue of tile i - 2 has read O[b] and
       // l[b] (which also means PV(i - 2) has consumed P[b])
-      TSF_STAMP(p, warp, 4 * i + 1);
+      TSF_STAMP(p, 12 + (warp), 4 * i + 1);
       if (i >= 2) {
         mbar_wait(&o_empty[b], ((i - 2) >> 1) & 1);
         tc_fence_after();
       }
-      TSF_STAMP(p, warp, 4 * i + 2);
+      TSF_STAMP(p, 12 + (warp), 4 * i + 2);
 #pragma unroll
       for (int c = 0; c < WIN / 2; c += 16)
         tmem_st_x16(tmem + lane_base + b * C::SLOT + C::COL_P + colstart / 2 + c, pk + c);
@@ -272,50 +308,53 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[b]);
-      TSF_STAMP(p, warp, 4 * i + 3);
+      TSF_STAMP(p, 12 + (warp), 4 * i + 3);
     }
-  } else {
-    // ===================== epilogue (warps 4-7) =====================
-    const uint32_t q4 = warp - C::W_EPI;                 // TMEM lane quarter
+  } else if (warp < C::W_CONV) {
+    // ===================== epilogue (warpgroup e = slot e: warps 4-7, 8-11) =====================
+    const uint32_t e = (warp - C::W_EPI) >> 2;          // slot of this warpgroup
+    const uint32_t q4 = warp & 3;                       // TMEM lane quarter
     const uint32_t r = q4 * 32 + lane;
     const uint32_t lane_base = (q4 * 32) << 16;
-    const uint32_t et = threadIdx.x - 32 * C::W_EPI;    // 0..127
+    const uint32_t et = threadIdx.x - 32 * (C::W_EPI + 4 * e);  // 0..127
     const bool row_ok = (int)r < rows_used;
     const int gi = (int)r / L, li = (int)r - gi * L;
     const bool dist = p.P > 1;
-    for (int i = 0; i < my_tiles; ++i) {
+    uint8_t* stg = sOut + e * C::TILE_BYTES;
+    const uint32_t bar_id = 1 + e;
+    const uint32_t tcol = tmem + lane_base + e * C::SLOT;
+    for (int i = (int)e; i < my_tiles; i += 2) {
       const int tile = blockIdx.x + i * gridDim.x;
-      const int s = i % NST, b = i & 1;
-      mbar_wait(&o_full[b], (i >> 1) & 1);
-      mbar_wait(&p_full[b], (i >> 1) & 1);               // l[b] written (release by the softmax warps)
+      const int s = i % NST;
+      const uint32_t ph = (i >> 1) & 1;
+      mbar_wait(&o_full[e], ph);
+      mbar_wait(&p_full[e], ph);                         // l[e] written (release by the softmax warps)
       mbar_wait(&in_conv[s], (i / NST) & 1);             // residual rows converted (release by the converter)
-      TSF_STAMP(p, warp, 4 * i);
+      TSF_STAMP(p, 12 + (warp), 4 * (i >> 1));
       tc_fence_after();
       float o[D];
 #pragma unroll
-      for (int c = 0; c < D; c += 32)
-        tmem_ld_x32(tmem + lane_base + b * C::SLOT + C::COL_O + c, reinterpret_cast<uint32_t*>(o + c));
-      const float l = lbuf[b * 128 + r];
+      for (int c = 0; c < D; c += 32) tmem_ld_x32(tcol + C::COL_O + c, reinterpret_cast<uint32_t*>(o + c));
+      const float l = lbuf[e * 128 + r];
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&o_empty[b]);
-      TSF_STAMP(p, warp, 4 * i + 1);
-      // staging tile i % 2 is free once the store of tile i - 2 has read it
-      uint8_t* stg = sOut + b * C::TILE_BYTES;
-      if (et == 0) bulk_wait_read1();
-      named_bar_sync(1, 128);
+      if (lane == 0) mbar_arrive(&o_empty[e]);
+      TSF_STAMP(p, 12 + (warp), 4 * (i >> 1) + 1);
+      // this warpgroup's staging tile is free once its previous store has read it
+      if (et == 0) bulk_wait_read0();
+      named_bar_sync(bar_id, 128);
       uint32_t nf = 0;
       if (row_ok) {
         const uint32_t orow = dist ? (uint32_t)((li / p.Kc) * (p.Kc * G) + (li % p.Kc) + p.Kc * gi) : r;
         nf = epilogue_row_stage<D, 128, 128>(o, 1.0f / l, sIn + s * C::TILE_BYTES, r, stg, orow);
       }
       report_nonfinite(p, nf);
-      TSF_STAMP(p, warp, 4 * i + 2);
+      TSF_STAMP(p, 12 + (warp), 4 * (i >> 1) + 2);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&in_empty[s]);        // the residual rows of this warp are read
-      named_bar_sync(1, 128);
+      named_bar_sync(bar_id, 128);
       if (et == 0) {
         const int a0 = (tile % p.tiles_a) * p.Ab, b0 = (tile / p.tiles_a) * p.Bb;
         if (dist) {
@@ -330,7 +369,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
         }
         bulk_commit();
       }
-      TSF_STAMP(p, warp, 4 * i + 3);
+      TSF_STAMP(p, 12 + (warp), 4 * (i >> 1) + 3);
     }
     if (et == 0) bulk_wait0();                           // every X_t store has landed
   }

@@ -342,7 +342,15 @@ static tsf_status launch_stream_t(tsf_handle* h, cudaStream_t st, const CUtensor
     using C = StreamCfg<D, WIN, NST>;
     int grid = h->num_sms;
     if (grid > p.num_tiles) grid = p.num_tiles;
-    return launch(h, attn_stream_kernel<D, WIN, NST>, grid, C::THREADS, C::SMEM, st, p, mx, mo, h->pm);
+    if constexpr (WIN == 32) {  // compact softmax for the short windows (C1 K = 4, C2 K = 8, C2 at P = 2 K = 16)
+      switch (p.L) {
+        case 4: return launch(h, attn_stream_kernel<D, WIN, NST, 4>, grid, C::THREADS, C::SMEM, st, p, mx, mo, h->pm);
+        case 8: return launch(h, attn_stream_kernel<D, WIN, NST, 8>, grid, C::THREADS, C::SMEM, st, p, mx, mo, h->pm);
+        case 16: return launch(h, attn_stream_kernel<D, WIN, NST, 16>, grid, C::THREADS, C::SMEM, st, p, mx, mo, h->pm);
+        default: break;
+      }
+    }
+    return launch(h, attn_stream_kernel<D, WIN, NST, 0>, grid, C::THREADS, C::SMEM, st, p, mx, mo, h->pm);
   }
   return fail(h, TSF_ERR_UNSUPPORTED, "stream kernel shape");
 }
@@ -384,27 +392,38 @@ static tsf_status dispatch_d(tsf_handle* h, bool packed, int win, int epi, cudaS
 
 // Attention over one view: q/k/v (q == k == v for the block stages).  The
 // output (o or y) uses the strides of `ov` (default: the input view's).
-// Joint attention with a block / causal mask (tsf_joint_attn): the flash kernel
-// with per-score masking (MASK = 1), default tile and exp settings.
-template <int D>
-static tsf_status launch_flash_masked(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
-                                      const CUtensorMap& mv, const AttnParams& p) {
+// Flash kernel with fixed tile / exp settings for the secondary calls: joint
+// attention with a block or causal mask (tsf_joint_attn, MASK = 1) and the
+// STORM epilogues (tsf_storm_attn), bf16 operands and P.
+template <int D, int EPI, int MASK>
+static tsf_status launch_flash_fixed(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
+                                     const CUtensorMap& mv, const AttnParams& p) {
   constexpr int SUB = (D == 64) ? 96 : 128, EMU = (D == 64) ? 6 : 0;
-  constexpr int NST = (D == 128) ? 2 : 4;
-  using C = FlashCfg<D, EPI_OUT16, NST, SUB, 1>;
+  constexpr bool SH = EpiTraits<EPI>::SHARED;
+  constexpr int NST = SH ? ((D == 128) ? 4 : 8) : ((D == 128) ? 2 : 4);
+  using C = FlashCfg<D, EPI, NST, SUB, 1>;
   const long long items = (long long)p.n_qpairs * p.A * p.B;
   if (items > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "too many work items");
   AttnParams pp = p;
   pp.num_items = (int)items;
   pp.flags = 0;
   const long long grid = items < h->num_sms ? items : h->num_sms;
-  return launch(h, attn_flash_kernel<D, EPI_OUT16, NST, EMU, SUB, 1, 1>, (int)grid, C::THREADS, C::SMEM, st, pp, mq,
+  return launch(h, attn_flash_kernel<D, EPI, NST, EMU, SUB, 1, MASK>, (int)grid, C::THREADS, C::SMEM, st, pp, mq,
                 mk, mv);
+}
+
+template <int D>
+static tsf_status launch_flash_special(tsf_handle* h, int epi, int mask, cudaStream_t st, const CUtensorMap& mq,
+                                       const CUtensorMap& mk, const CUtensorMap& mv, const AttnParams& p) {
+  if (mask) return launch_flash_fixed<D, EPI_OUT16, 1>(h, st, mq, mk, mv, p);
+  if (epi == EPI_STORM_X) return launch_flash_fixed<D, EPI_STORM_X, 0>(h, st, mq, mk, mv, p);
+  return launch_flash_fixed<D, EPI_STORM_S, 0>(h, st, mq, mk, mv, p);
 }
 
 static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, const void* k, const void* vv, int epi,
                                 void* o, float* y, cudaStream_t st, const View* ov = nullptr,
-                                const DistOut* dist = nullptr, int mask = 0) {
+                                const DistOut* dist = nullptr, int mask = 0, const View* kvv = nullptr,
+                                float gate = 0.f) {
   if (!ov) ov = &v;
   h->use_pm = false;
   const int d = h->d;
@@ -436,9 +455,13 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
   p.trace = h->trace;
 #endif
   const bool f16 = (epi == EPI_BLOCK_S);  // X_t lives in fp16; x (BLOCK_T) arrives bf16
-  const bool packed = v.L <= 128 && mask == 0;
+  const bool special = mask != 0 || epi == EPI_STORM_X || epi == EPI_STORM_S;  // flash kernel, fixed settings
+  const bool packed = v.L <= 128 && !special;
   p.mask_mode = mask;
   p.mask_n = h->N;
+  if (!kvv) kvv = &v;  // keys / values: the query view unless cross-attention
+  p.Lk = kvv->L;
+  p.gate = gate;
   int win = 128;
   CUtensorMap mq, mk, mv, mo;
   memset(&mo, 0, sizeof mo);
@@ -476,16 +499,16 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
     }
   } else {
     p.n_qpairs = (v.L + 255) / 256;
-    const int sub = flash_sub(d);  // K/V tile rows
-    p.nkv = (v.L + sub - 1) / sub;
+    const int sub = special ? ((d == 64) ? 96 : 128) : flash_sub(d);  // K/V tile rows
+    p.nkv = (kvv->L + sub - 1) / sub;
     if ((s = make_map(h, &mq, q, d, v, 128, 1, 1, f16)) != TSF_OK) return s;
-    if ((s = make_map(h, &mk, k, d, v, sub, 1, 1, f16)) != TSF_OK) return s;
-    if ((s = make_map(h, &mv, vv, d, v, sub, 1, 1, f16)) != TSF_OK) return s;
-    if (mask) {
+    if ((s = make_map(h, &mk, k, d, *kvv, sub, 1, 1, f16)) != TSF_OK) return s;
+    if ((s = make_map(h, &mv, vv, d, *kvv, sub, 1, 1, f16)) != TSF_OK) return s;
+    if (special) {
       switch (d) {
-        case 32: return launch_flash_masked<32>(h, st, mq, mk, mv, p);
-        case 64: return launch_flash_masked<64>(h, st, mq, mk, mv, p);
-        default: return launch_flash_masked<128>(h, st, mq, mk, mv, p);
+        case 32: return launch_flash_special<32>(h, epi, mask, st, mq, mk, mv, p);
+        case 64: return launch_flash_special<64>(h, epi, mask, st, mq, mk, mv, p);
+        default: return launch_flash_special<128>(h, epi, mask, st, mq, mk, mv, p);
       }
     }
   }
@@ -850,6 +873,31 @@ tsf_status tsf_joint_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, c
   const View jv{h->K * h->N, h->H, 1, (long long)h->H * h->d, (long long)h->d, (long long)h->K * h->N * h->H * h->d};
   StageTimer tm(h, st, 5);
   s = run_attention(h, jv, q, k, v, EPI_OUT16, o, nullptr, st, nullptr, nullptr, mask);
+  tm.done();
+  return s;
+}
+
+tsf_status tsf_storm_attn(tsf_handle* h, const tsf_bf16* u, const tsf_bf16* ctx, int M, double sigma,
+                          double sigma_data, float* y, void* stream) {
+  if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
+  h->launches = 0;
+  if (M < 1) return fail(h, TSF_ERR_CONFIG, "M must be >= 1");
+  if (!(sigma_data > 0.0) || !(sigma >= 0.0) || !std::isfinite(sigma))
+    return fail(h, TSF_ERR_CONFIG, "need sigma >= 0 (finite) and sigma_data > 0");
+  if (h->world != 1) return fail(h, TSF_ERR_UNSUPPORTED, "STORM attention runs on single-GPU handles");
+  const int B = h->K, N = h->N, H = h->H, d = h->d;
+  const size_t ubytes = (size_t)B * N * H * d * 2, cbytes = (size_t)B * M * H * d * 2, ybytes = (size_t)B * N * H * d * 4;
+  tsf_status s = check_ptrs(h, {u}, y, ubytes, ybytes);
+  if (s != TSF_OK) return s;
+  if ((s = check_ptrs(h, {ctx}, y, cbytes, ybytes)) != TSF_OK) return s;
+  const double g = sigma * sigma / (sigma * sigma + sigma_data * sigma_data);  // noise gate (reading G18)
+  cudaStream_t st = (cudaStream_t)stream;
+  const View vu = spatial_view(B, N, H, d);                                    // groups (h, b), axis n
+  const View vc{M, H, B, (long long)H * d, (long long)d, (long long)M * H * d};  // groups (h, b), axis m
+  StageTimer tm(h, st, 6);
+  // y = u + g Cross(u, ctx, ctx)  then  y += (1 - g) Self(u, u, u)
+  s = run_attention(h, vu, u, ctx, ctx, EPI_STORM_X, nullptr, y, st, nullptr, nullptr, 0, &vc, (float)g);
+  if (s == TSF_OK) s = run_attention(h, vu, u, u, u, EPI_STORM_S, nullptr, y, st, nullptr, nullptr, 0, nullptr, (float)(1.0 - g));
   tm.done();
   return s;
 }

@@ -265,7 +265,7 @@ def test_block_large_magnitude_x(tsf_lib, factor):
 
 
 def test_block_nonfinite_x_t_is_reported(tsf_lib):
-    """|x| = 4e4: X_t = x + T(x) ~ 8e4 exceeds fp16 -> TSF_ERR_NUMERIC, not silent inf."""
+    """|x| = 4e4: X_t = x + T(x) = 8e4 exceeds fp16 -> TSF_ERR_NUMERIC, not silent inf."""
     K, N, H, d = 4, 64, 2, 32
     layer = tsf_lib.Layer(K, N, H, d)
     x = torch.full((K, N, H, d), 4.0e4, dtype=torch.bfloat16, device="cuda")
@@ -280,9 +280,11 @@ def test_block_nonfinite_x_t_is_reported(tsf_lib):
     with pytest.raises(tsf_lib.TsfError) as e:
         layer.block_host(xh, yh)
     assert e.value.status == tsf_lib.TSF_ERR_NUMERIC
-    # in range: no error (|x| = 1e4 -> X_t = 2e4 < 65504)
-    layer.block(torch.full((K, N, H, d), 1.0e4, dtype=torch.bfloat16, device="cuda"))
+    # in range: no error, and the closed form (equal keys: T(x) = x, S(X_t) = X_t)
+    # holds exactly: x = 100 -> X_t = 200 -> y = 400
+    y = layer.block(torch.full((K, N, H, d), 100.0, dtype=torch.bfloat16, device="cuda"))
     layer.sync()
+    assert torch.all(y == 400.0)
     # a flash-kernel temporal stage (K > 128) reports it too
     big = tsf_lib.Layer(200, 2, 2, 64)
     xb = torch.zeros((200, 2, 2, 64), dtype=torch.bfloat16, device="cuda")

@@ -341,3 +341,45 @@ def test_oracle_rejects_non_finite():
     q[0, 0, 0, 0] = np.nan
     with pytest.raises(ValueError):
         oracle.temporal(q, q, q)
+
+
+# --- STORM per-layer attention (NEXT-3) ------------------------------------
+
+def test_noise_gate_spec_examples():
+    """SPEC.md S:233-235 printed values; monotone, g(0) = 0, g -> 1."""
+    assert oracle.noise_gate(0.0, 0.7) == 0.0
+    assert oracle.noise_gate(0.7, 0.7) == 0.5
+    assert abs(oracle.noise_gate(2.1, 0.7) - 0.9) < 1e-15
+    gs = [oracle.noise_gate(s, 1.0) for s in np.linspace(0, 50, 101)]
+    assert all(b > a for a, b in zip(gs, gs[1:])) and gs[-1] > 0.999
+    with pytest.raises(ValueError):
+        oracle.noise_gate(1.0, 0.0)
+
+
+def test_cross_matches_library_sdpa():
+    """Cross-attention with query and key lengths that differ = torch SDPA fp64."""
+    B, N, M, H, d = 2, 7, 5, 3, 8
+    q, k, v = rand(B, N, H, d), rand(B, M, H, d), rand(B, M, H, d)
+    g = lambda a: torch.from_numpy(np.ascontiguousarray(a.transpose(0, 2, 1, 3)))
+    ref = torch.nn.functional.scaled_dot_product_attention(g(q), g(k), g(v)).numpy().transpose(0, 2, 1, 3)
+    np.testing.assert_allclose(oracle.cross(q, k, v), ref, rtol=0, atol=1e-12)
+
+
+def test_storm_special_cases():
+    B, N, M, H, d = 2, 6, 4, 2, 8
+    u, ctx = rand(B, N, H, d), rand(B, M, H, d)
+    # sigma = 0: pure spatial self-attention on the current state (the block's spatial stage)
+    np.testing.assert_allclose(oracle.storm_attention(u, ctx, 0.0, 1.0), u + oracle.spatial(u, u, u),
+                               rtol=0, atol=1e-12)
+    # one context token: cross-attention returns it exactly (single key, weight 1)
+    c1 = rand(B, 1, H, d)
+    g = oracle.noise_gate(2.0, 1.0)
+    want = u + (1 - g) * oracle.spatial(u, u, u) + g * np.broadcast_to(c1, u.shape)
+    np.testing.assert_allclose(oracle.storm_attention(u, c1, 2.0, 1.0), want, rtol=0, atol=1e-12)
+    # context = the state itself: cross = self, y = u + spatial(u) for every sigma
+    np.testing.assert_allclose(oracle.storm_attention(u, u, 3.0, 1.0), u + oracle.spatial(u, u, u),
+                               rtol=0, atol=1e-12)
+    # permuting the context tokens changes nothing (keys are a set)
+    perm = np.random.default_rng(3).permutation(M)
+    np.testing.assert_allclose(oracle.storm_attention(u, ctx[:, perm], 1.5, 1.0),
+                               oracle.storm_attention(u, ctx, 1.5, 1.0), rtol=0, atol=1e-12)

@@ -4,7 +4,8 @@
     TSF_LIB=paper_2604_16590_b200/libtsf_trace.so python tools/trace_flash.py [K N H d]
 
 Softmax warp stamps per sub-step i: 0 loop top, 1 S ready (s_full), 2 S in
-registers, 3 row max done, 4 P stored, 5 p_full arrived.  MMA warp (9): per
+registers, 3 row max done, 4 exponentials done, 5 P stored (after the wait for
+PV(G-1)), 6 p_full arrived.  MMA warp (9): per
 score tile n = 2i + t: 2n p_full seen, 2n+1 PV(n) and S(n + NB) issued.
 """
 import ctypes
@@ -43,22 +44,22 @@ def main():
     nsub = (N + sub - 1) // sub
     t0 = a[a > 0].min()
     print(f"{what} TSF_EMU={os.environ.get('TSF_EMU', 'default')} nsub={nsub}  kernel span (CTA0 stamps) {a.max() - t0} cycles")
-    phases = ["wait S", "ld S", "max", "exp+st", "arrive", "to next"]
-    split = int(os.environ.get("TSF_SPLIT", "2" if d == 64 else "1"))
+    phases = ["wait S", "ld S", "max", "exp", "PVwait+st", "arrive", "to next"]
+    split = int(os.environ.get("TSF_SPLIT", "1"))
     wmma = 8 * split + 1
     for w in range(8 * split):
-        s = a[w, :6 * nsub].reshape(nsub, 6)
+        s = a[w, :7 * nsub].reshape(nsub, 7)
         dif = np.diff(s, axis=1)
-        nxt = s[1:, 0] - s[:-1, 5]
+        nxt = s[1:, 0] - s[:-1, 6]
         per = dif.mean(0).tolist() + [nxt.mean()]
-        tot = (s[-1, 5] - s[0, 0]) / nsub
+        tot = (s[-1, 6] - s[0, 0]) / nsub
         print(f"warp {w}: cycles/sub-step {tot:7.1f} | " + " ".join(f"{p} {v:6.1f}" for p, v in zip(phases, per)))
     m = a[wmma, :4 * nsub].reshape(2 * nsub, 2)
     print(f"MMA warp {wmma}: mean cycles p_full->issued {np.diff(m, axis=1).mean():.1f}, "
           f"issued->next p_full {(m[1:, 0] - m[:-1, 1]).mean():.1f}")
     print("first sub-steps, warp 0 and warp 4 (relative to kernel start):")
     for i in range(min(6, nsub)):
-        print(i, (a[0, 6 * i:6 * i + 6] - t0).tolist(), (a[4 * split, 6 * i:6 * i + 6] - t0).tolist(),
+        print(i, (a[0, 7 * i:7 * i + 7] - t0).tolist(), (a[4 * split, 7 * i:7 * i + 7] - t0).tolist(),
               (a[wmma, 4 * i:4 * i + 4] - t0).tolist())
     os.makedirs("gpurun_out", exist_ok=True)
     np.save("gpurun_out/trace_flash.npy", a)

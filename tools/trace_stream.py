@@ -3,10 +3,11 @@
     python -m paper_2604_16590_b200.build --trace
     TSF_LIB=paper_2604_16590_b200/libtsf_trace.so python tools/trace_stream.py [K N H d]
 
-Stamps (clock64, CTA 0): producer warp 8: stage free (per tile); converter
-warp 11: tile landed / converted; QK warp 9 and PV warp 10: operands ready;
-softmax warp 0: S ready / P computed / slot free / P handed over; epilogue
-warp 4: O ready / O read / staging written / store issued.
+Stamps (clock64, CTA 0, trace row 12 + warp): producer warp 16: stage free
+(per tile); converter warps 12-15: tile landed / converted; QK warp 17 and PV
+warp 18: operands ready; softmax warp 0: S ready / P computed / slot free /
+P handed over; epilogue warps 4 / 8 (even / odd tiles): O ready / O read /
+staging written / store issued.
 """
 import ctypes
 import os
@@ -39,28 +40,31 @@ def main():
     torch.cuda.synchronize()
     L.tsf_trace_read(layer._h, buf, n)
     a = np.frombuffer(buf, dtype=np.uint64).reshape(32, PER_WARP).astype(np.int64)
-    nt = int(np.count_nonzero(a[9]))
-    t0 = a[a > 0].min()
+    R = 12                                              # the kernel stamps warp w into row 12 + w
+    nt = int(np.count_nonzero(a[R + 17]))
+    t0 = a[R:][a[R:] > 0].min()
     r = lambda v: (v - t0).tolist()
     print(f"tiles in CTA0: {nt}")
-    print("producer stage-free  :", r(a[8, :nt]))
-    print("converter landed     :", r(a[11, 0:2 * nt:2]))
-    print("converter done       :", r(a[11, 1:2 * nt:2]))
-    print("QK issue             :", r(a[9, :nt]))
-    sm = a[0, :4 * nt].reshape(nt, 4)
+    print("producer stage-free  :", r(a[R + 16, :nt]))
+    conv = [a[R + 12 + (i % 4), 2 * (i // 4):2 * (i // 4) + 2] for i in range(nt)]
+    print("converter landed     :", r(np.array([c[0] for c in conv])))
+    print("converter done       :", r(np.array([c[1] for c in conv])))
+    print("QK issue             :", r(a[R + 17, :nt]))
+    sm = a[R + 0, :4 * nt].reshape(nt, 4)
     print("softmax S ready      :", r(sm[:, 0]))
     print("softmax P computed   :", r(sm[:, 1]))
     print("softmax slot free    :", r(sm[:, 2]))
     print("softmax P handed     :", r(sm[:, 3]))
-    print("PV issue             :", r(a[10, :nt]))
-    ep = a[4, :4 * nt].reshape(nt, 4)
+    print("PV issue             :", r(a[R + 18, :nt]))
+    ep = np.array([a[R + 4 + 4 * (i % 2), 4 * (i // 2):4 * (i // 2) + 4] for i in range(nt)])
     print("epilogue O ready     :", r(ep[:, 0]))
     print("epilogue O read      :", r(ep[:, 1]))
     print("epilogue staged      :", r(ep[:, 2]))
     print("epilogue store issued:", r(ep[:, 3]))
     span = ep[-1, 3] - t0
+    cv = np.array([c[1] - c[0] for c in conv])
     print(f"span {span} cycles, {span / nt:.0f} per tile; mean softmax {np.mean(sm[:, 3] - sm[:, 0]):.0f}, "
-          f"epilogue {np.mean(ep[:, 3] - ep[:, 0]):.0f}, convert {np.mean(a[11, 1:2 * nt:2] - a[11, 0:2 * nt:2]):.0f}")
+          f"epilogue {np.mean(ep[:, 3] - ep[:, 0]):.0f}, convert {cv.mean():.0f}")
 
 
 if __name__ == "__main__":
