@@ -111,6 +111,37 @@ tsf_status tsf_joint_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, c
 tsf_status tsf_storm_attn(tsf_handle* h, const tsf_bf16* u, const tsf_bf16* ctx, int M, double sigma,
                           double sigma_data, float* y, void* stream);
 
+/* Parameters of the full TimeSformer divided block (tsf_full_block), device
+ * pointers.  D = H*d, F = MLP hidden size.  Weights bf16 in the [out, in]
+ * layout (nn.Linear), biases and LayerNorm gains/shifts fp32. */
+typedef struct {
+  const float* ln_t_g; const float* ln_t_b;          /* [D]: pre-LN of the temporal stage */
+  const tsf_bf16* w_qkv_t; const float* b_qkv_t;     /* [3D, D], [3D]: rows q | k | v */
+  const tsf_bf16* w_o_t; const float* b_o_t;         /* [D, D], [D] */
+  const float* ln_s_g; const float* ln_s_b;          /* spatial stage, same shapes */
+  const tsf_bf16* w_qkv_s; const float* b_qkv_s;
+  const tsf_bf16* w_o_s; const float* b_o_s;
+  const float* ln_m_g; const float* ln_m_b;          /* [D]: pre-LN of the MLP */
+  const tsf_bf16* w_1; const float* b_1;             /* [F, D], [F] */
+  const tsf_bf16* w_2; const float* b_2;             /* [D, F], [D] */
+  int F;
+} tsf_block_weights;
+
+/* Full TimeSformer divided space-time block (the layers around
+ * the factorized attention of P:64, reading G21 in DESIGN.md):
+ *   (q,k,v) = split(LN_t(x) Wqkv_t^T + b);   X_t = x + T(q,k,v) Wo_t^T + bo_t
+ *   (q,k,v) = split(LN_s(X_t) Wqkv_s^T + b); X_s = X_t + S(q,k,v) Wo_s^T + bo_s
+ *   y = X_s + GELU(LN_m(X_s) W1^T + b1) W2^T + b2
+ * x: bf16 [K, N, H, d] (= [K*N, D] tokens); y: fp32 [K, N, H, d].  Residual
+ * stream fp32; LN outputs, q/k/v, attention outputs and the GELU output bf16;
+ * every GEMM bf16 x bf16 -> fp32 on tcgen05 with the bias / GELU / residual
+ * fused into its epilogue; attention = the tsf_temporal_attn /
+ * tsf_spatial_attn kernels reading q, k, v in place from the QKV GEMM output.
+ * Needs D % 128 == 0, F % 128 == 0, D <= 8192; single-GPU handles.  The
+ * first call allocates the activation workspace (~2*T*(4D + F) bytes + 8*T*D
+ * for T = K*N tokens), kept until tsf_destroy. */
+tsf_status tsf_full_block(tsf_handle* h, const tsf_block_weights* w, const tsf_bf16* x, float* y, void* stream);
+
 /* Divided space-time block, temporal then spatial ("followed by"), with
  * identity projections and residual weight 1 (readings G1, G5):
  *   X_t = x + T(x, x, x);   y = X_t + S(X_t, X_t, X_t).
@@ -214,7 +245,8 @@ int tsf_world_size(const tsf_handle* h);
  * returns the summed milliseconds and the number of recorded launches of
  * stage 0 = temporal attention, 1 = spatial attention, 2 = reshard
  * (all-to-all + unpack), 3 = host<->device copies, 4 = tsf_transpose,
- * 5 = tsf_joint_attn, 6 = tsf_storm_attn. */
+ * 5 = tsf_joint_attn, 6 = tsf_storm_attn, 7 = tsf_full_block GEMMs and
+ * LayerNorms (its attention kernels are recorded as stages 0 and 1). */
 tsf_status tsf_set_timing(tsf_handle* h, int enable);
 tsf_status tsf_stage_ms(tsf_handle* h, int stage, float* total_ms, int* n_records);
 

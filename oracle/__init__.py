@@ -32,6 +32,10 @@ from .attention import (  # noqa: F401
     noise_gate,
     cross,
     storm_attention,
+    layer_norm,
+    linear,
+    gelu,
+    full_block,
     temporal_rows,
     spatial_rows,
     block_rows,

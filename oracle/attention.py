@@ -330,3 +330,56 @@ def reshard_s2t(frame_shards: Sequence[np.ndarray]) -> list:
     full = np.concatenate(list(frame_shards), axis=0)
     P = len(frame_shards)
     return [shard_tokens(full, P, p).copy() for p in range(P)]
+
+
+# ---------------------------------------------------------------------------
+# full TimeSformer divided block: per-stage projections,
+# pre-LayerNorm, MLP around the factorized attention (reading G21)
+# ---------------------------------------------------------------------------
+
+def layer_norm(x: np.ndarray, gamma: np.ndarray, beta: np.ndarray, eps: float = 1e-5) -> np.ndarray:
+    """(x - mean) / sqrt(var + eps) * gamma + beta over the last axis (biased variance)."""
+    mu = x.mean(axis=-1, keepdims=True)
+    var = ((x - mu) ** 2).mean(axis=-1, keepdims=True)
+    return (x - mu) / np.sqrt(var + eps) * gamma + beta
+
+
+def linear(x: np.ndarray, w: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """x W^T + b with W in the [out, in] layout."""
+    return np.matmul(x, w.T) + b
+
+
+def gelu(x: np.ndarray) -> np.ndarray:
+    """GELU, exact form 0.5 x (1 + erf(x / sqrt 2))."""
+    from scipy.special import erf
+    return 0.5 * x * (1.0 + erf(x / math.sqrt(2.0)))
+
+
+def full_block(x: np.ndarray, p: dict) -> np.ndarray:
+    """TimeSformer divided space-time block (reading G21), x [K, N, H, d]:
+
+        (q, k, v) = split(LN_t(x) Wqkv_t^T + bqkv_t);   X_t = x + T(q, k, v) Wo_t^T + bo_t
+        (q, k, v) = split(LN_s(X_t) Wqkv_s^T + bqkv_s); X_s = X_t + S(q, k, v) Wo_s^T + bo_s
+        y = X_s + GELU(LN_m(X_s) W1^T + b1) W2^T + b2
+
+    T / S are temporal / spatial attention ("followed by"), split takes
+    columns [0, D), [D, 2D), [2D, 3D) as q, k, v with D = H d and head h at
+    columns [h d, (h+1) d) of each.  p holds float64 arrays keyed as in
+    synth.make_block_params.
+    """
+    _check(x)
+    K, N, H, d = x.shape
+    D = H * d
+    xs = x.reshape(K, N, D)
+
+    def qkv(h, w, b):
+        t = linear(h, w, b)
+        return tuple(t[..., i * D:(i + 1) * D].reshape(K, N, H, d) for i in range(3))
+
+    q, k, v = qkv(layer_norm(xs, p["ln_t_g"], p["ln_t_b"]), p["w_qkv_t"], p["b_qkv_t"])
+    xt = xs + linear(temporal(q, k, v).reshape(K, N, D), p["w_o_t"], p["b_o_t"])
+    q, k, v = qkv(layer_norm(xt, p["ln_s_g"], p["ln_s_b"]), p["w_qkv_s"], p["b_qkv_s"])
+    xsp = xt + linear(spatial(q, k, v).reshape(K, N, D), p["w_o_s"], p["b_o_s"])
+    m = gelu(linear(layer_norm(xsp, p["ln_m_g"], p["ln_m_b"]), p["w_1"], p["b_1"]))
+    y = xsp + linear(m, p["w_2"], p["b_2"])
+    return y.reshape(K, N, H, d)

@@ -41,6 +41,7 @@ SIGNATURES = [
     ("tsf_spatial_attn", _I, [_P, _P, _P, _P, _P, _P]),
     ("tsf_joint_attn", _I, [_P, _P, _P, _P, _P, _I, _P]),
     ("tsf_storm_attn", _I, [_P, _P, _P, _I, ctypes.c_double, ctypes.c_double, _P, _P]),
+    ("tsf_full_block", _I, [_P, _P, _P, _P, _P]),
     ("tsf_spacetime_block", _I, [_P, _P, _P, _P]),
     ("tsf_spacetime_block_host", _I, [_P, _P, _P, _P]),
     ("tsf_destroy", None, [_P]),
@@ -59,6 +60,16 @@ SIGNATURES = [
 ]
 
 _lib = None
+
+
+BLOCK_WEIGHT_FIELDS = ["ln_t_g", "ln_t_b", "w_qkv_t", "b_qkv_t", "w_o_t", "b_o_t",
+                       "ln_s_g", "ln_s_b", "w_qkv_s", "b_qkv_s", "w_o_s", "b_o_s",
+                       "ln_m_g", "ln_m_b", "w_1", "b_1", "w_2", "b_2"]
+
+
+class BlockWeights(ctypes.Structure):
+    """tsf_block_weights (include/tsf.h): device pointers + the MLP width F."""
+    _fields_ = [(n, ctypes.c_void_p) for n in BLOCK_WEIGHT_FIELDS] + [("F", ctypes.c_int)]
 
 
 class TsfError(RuntimeError):
@@ -221,6 +232,31 @@ class Layer:
         _need(out, torch.float32, (self.K, self.N, self.H, self.d), "out")
         _check(lib().tsf_storm_attn(self._h, u.data_ptr(), ctx.data_ptr(), int(ctx.shape[1]), float(sigma),
                                     float(sigma_data), out.data_ptr(), _stream_ptr(stream)), self._h)
+        return out
+
+    def full_block(self, x, weights: dict, out=None, stream=None):
+        """tsf_full_block: the full divided block (pre-LN, QKV / O projections, MLP) around
+        the factorized attention.  weights: name -> CUDA tensor (bf16 [out, in] weights,
+        fp32 vectors), names as in BLOCK_WEIGHT_FIELDS.  x bf16 [K, N, H, d] -> y fp32."""
+        import torch
+        shp = (self.K, self.N, self.H, self.d)
+        _need(x, torch.bfloat16, shp, "x")
+        D = self.H * self.d
+        F = weights["w_1"].shape[0]
+        want = {"w_qkv_t": (3 * D, D), "w_o_t": (D, D), "w_qkv_s": (3 * D, D), "w_o_s": (D, D),
+                "w_1": (F, D), "w_2": (D, F), "b_qkv_t": (3 * D,), "b_qkv_s": (3 * D,), "b_1": (F,)}
+        st = BlockWeights()
+        for n in BLOCK_WEIGHT_FIELDS:
+            t = weights[n]
+            _need(t, torch.bfloat16 if n.startswith("w_") else torch.float32, want.get(n, (D,)), n)
+            if not t.is_cuda:
+                raise ValueError(f"{n} must be a CUDA tensor")
+            setattr(st, n, t.data_ptr())
+        st.F = F
+        out = torch.empty(shp, dtype=torch.float32, device=x.device) if out is None else out
+        _need(out, torch.float32, shp, "out")
+        _check(lib().tsf_full_block(self._h, ctypes.byref(st), x.data_ptr(), out.data_ptr(), _stream_ptr(stream)),
+               self._h)
         return out
 
     def block(self, x, out=None, stream=None):

@@ -20,6 +20,7 @@
 #include "attn_flash.cuh"
 #include "attn_packed.cuh"
 #include "attn_stream.cuh"
+#include "gemm.cuh"
 #include "layout.cuh"
 
 using namespace tsf;
@@ -80,6 +81,9 @@ struct tsf_handle {
   // every virtual rank's buffer back to back; sim_mode 1 = NCCL byte plan with
   // device copies in place of send/recv, 2 = fused scatter
   bool sim = false;
+  // full-block activation workspace (tsf_full_block), allocated on first use
+  void* fb = nullptr;
+  size_t fb_bytes = 0;
 };
 constexpr int HOST_CHUNKS = 4;
 
@@ -594,7 +598,8 @@ static tsf_status alloc_workspace(tsf_handle* h) {
 }
 
 static void free_workspace(tsf_handle* h) {
-  for (void* p : {(void*)h->xt, (void*)h->rxt, (void*)h->uxt, (void*)h->xdev, (void*)h->ydev, (void*)h->scratch})
+  for (void* p : {(void*)h->xt, (void*)h->rxt, (void*)h->uxt, (void*)h->xdev, (void*)h->ydev, (void*)h->scratch,
+                  h->fb})
     if (p) cudaFree(p);
   if (h->nf_host) cudaFreeHost(const_cast<unsigned int*>(h->nf_host));
   h->xt = h->rxt = h->uxt = nullptr;
@@ -602,6 +607,7 @@ static void free_workspace(tsf_handle* h) {
   h->ydev = nullptr;
   h->scratch = nullptr;
   h->nf_host = nullptr;
+  h->fb = nullptr;
 }
 
 // ---------------------------------------------------------------------------
@@ -900,6 +906,176 @@ tsf_status tsf_storm_attn(tsf_handle* h, const tsf_bf16* u, const tsf_bf16* ctx,
   if (s == TSF_OK) s = run_attention(h, vu, u, u, u, EPI_STORM_S, nullptr, y, st, nullptr, nullptr, 0, nullptr, (float)(1.0 - g));
   tm.done();
   return s;
+}
+
+// ---------------------------------------------------------------------------
+// Full divided block (NEXT-1): LayerNorm, tcgen05 GEMMs with fused epilogues,
+// and the attention kernels on strided q / k / v views of the QKV output.
+// ---------------------------------------------------------------------------
+}  // extern "C"
+static tsf_status make_map2d(tsf_handle* h, CUtensorMap* m, const void* base, long long rows, long long cols,
+                             int box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return fail(h, TSF_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(h, TSF_ERR_CUDA, "cuTensorMapEncodeTiled (GEMM) failed: " + std::to_string((int)r));
+  return TSF_OK;
+}
+
+template <int BN, int EPI>
+static tsf_status launch_gemm(tsf_handle* h, cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mw,
+                              const GemmParams& p) {
+  using C = GemmCfg<BN>;
+  const int tiles = p.tiles_m * p.tiles_n;
+  cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  if (e != cudaSuccess) return fail(h, TSF_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  gemm_kernel<BN, EPI><<<tiles < h->num_sms ? tiles : h->num_sms, 192, C::SMEM, st>>>(ma, mw, p);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(h, TSF_ERR_CUDA, std::string("GEMM launch: ") + cudaGetErrorString(e));
+  h->launches++;
+  return TSF_OK;
+}
+
+// C[M, N] = A[M, K] W[N, K]^T + bias (+ epilogue); N % 128 == 0, K % 64 == 0
+static tsf_status gemm(tsf_handle* h, cudaStream_t st, int epi, const void* A, const void* W, const float* bias,
+                       const void* res, void* Cout, long long M, int N, int K) {
+  if (N % 128 || K % 64) return fail(h, TSF_ERR_UNSUPPORTED, "GEMM needs N % 128 == 0 and K % 64 == 0");
+  const int BN = (N % 256 == 0) ? 256 : 128;
+  CUtensorMap ma, mw;
+  tsf_status s;
+  if ((s = make_map2d(h, &ma, A, M, K, 128)) != TSF_OK) return s;
+  if ((s = make_map2d(h, &mw, W, N, K, BN)) != TSF_OK) return s;
+  GemmParams p{};
+  p.M = (int)M; p.N = N; p.K = K;
+  p.bias = bias; p.res = res; p.c = Cout; p.ldc = N;
+  p.tiles_m = (int)((M + 127) / 128);
+  p.tiles_n = N / BN;
+  StageTimer tm(h, st, 7);
+  if (BN == 256) {
+    switch (epi) {
+      case GEPI_BIAS_BF16: s = launch_gemm<256, GEPI_BIAS_BF16>(h, st, ma, mw, p); break;
+      case GEPI_GELU_BF16: s = launch_gemm<256, GEPI_GELU_BF16>(h, st, ma, mw, p); break;
+      case GEPI_RES_F32: s = launch_gemm<256, GEPI_RES_F32>(h, st, ma, mw, p); break;
+      default: s = launch_gemm<256, GEPI_RESB_F32>(h, st, ma, mw, p); break;
+    }
+  } else {
+    switch (epi) {
+      case GEPI_BIAS_BF16: s = launch_gemm<128, GEPI_BIAS_BF16>(h, st, ma, mw, p); break;
+      case GEPI_GELU_BF16: s = launch_gemm<128, GEPI_GELU_BF16>(h, st, ma, mw, p); break;
+      case GEPI_RES_F32: s = launch_gemm<128, GEPI_RES_F32>(h, st, ma, mw, p); break;
+      default: s = launch_gemm<128, GEPI_RESB_F32>(h, st, ma, mw, p); break;
+    }
+  }
+  tm.done();
+  return s;
+}
+
+template <typename IN>
+static tsf_status layer_norm(tsf_handle* h, cudaStream_t st, const IN* x, const float* g, const float* b,
+                             __nv_bfloat16* y, long long rows, int D) {
+  const int blocks = (int)((rows + 7) / 8);
+  const int need = (D + 255) / 256;  // 8-element chunks per lane
+  StageTimer tm(h, st, 7);
+  if (need <= 1) layernorm_kernel<IN, 1><<<blocks, 256, 0, st>>>(x, g, b, y, rows, D);
+  else if (need <= 2) layernorm_kernel<IN, 2><<<blocks, 256, 0, st>>>(x, g, b, y, rows, D);
+  else if (need <= 4) layernorm_kernel<IN, 4><<<blocks, 256, 0, st>>>(x, g, b, y, rows, D);
+  else if (need <= 8) layernorm_kernel<IN, 8><<<blocks, 256, 0, st>>>(x, g, b, y, rows, D);
+  else if (need <= 16) layernorm_kernel<IN, 16><<<blocks, 256, 0, st>>>(x, g, b, y, rows, D);
+  else layernorm_kernel<IN, 32><<<blocks, 256, 0, st>>>(x, g, b, y, rows, D);
+  tm.done();
+  TSF_CUDA(h, cudaGetLastError());
+  h->launches++;
+  return TSF_OK;
+}
+
+extern "C" {
+tsf_status tsf_full_block(tsf_handle* h, const tsf_block_weights* w, const tsf_bf16* x, float* y, void* stream) {
+  if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
+  h->launches = 0;
+  if (!w) return fail(h, TSF_ERR_CONFIG, "null weights");
+  if (h->world != 1) return fail(h, TSF_ERR_UNSUPPORTED, "the full block runs on single-GPU handles");
+  const int K = h->K, N = h->N, H = h->H, d = h->d, D = H * d, F = w->F;
+  const long long T = (long long)K * N;
+  if (D % 128 || D > 8192 || F < 128 || F % 128) return fail(h, TSF_ERR_UNSUPPORTED, "need D = H*d % 128 == 0 (<= 8192) and F % 128 == 0");
+  const void* ptrs[] = {w->ln_t_g, w->ln_t_b, w->w_qkv_t, w->b_qkv_t, w->w_o_t, w->b_o_t, w->ln_s_g, w->ln_s_b,
+                        w->w_qkv_s, w->b_qkv_s, w->w_o_s, w->b_o_s, w->ln_m_g, w->ln_m_b, w->w_1, w->b_1, w->w_2, w->b_2};
+  for (const void* p : ptrs)
+    if (!p || !aligned16(p)) return fail(h, TSF_ERR_CONFIG, "weight pointer null or not 16-byte aligned");
+  tsf_status s = check_ptrs(h, {x}, y, (size_t)T * D * 2, (size_t)T * D * 4);
+  if (s != TSF_OK) return s;
+  // workspace: hb bf16 [T, D] | qkv bf16 [T, 3D] | o bf16 [T, D] | m bf16 [T, F] | xt fp32 [T, D] | xs fp32 [T, D]
+  const size_t need = (size_t)T * (2 * D + 6 * D + 2 * D + 2 * (size_t)F + 4 * D + 4 * D) + 4 * 256;
+  if (h->fb_bytes < need) {
+    if (h->fb) cudaFree(h->fb);
+    h->fb = nullptr;
+    h->fb_bytes = 0;
+    if (cudaMalloc(&h->fb, need) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(h, TSF_ERR_NOMEM, "full-block workspace cudaMalloc failed");
+    }
+    h->fb_bytes = need;
+  }
+  auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+  char* base = static_cast<char*>(h->fb);
+  __nv_bfloat16* hb = reinterpret_cast<__nv_bfloat16*>(base);
+  __nv_bfloat16* qkv = reinterpret_cast<__nv_bfloat16*>(base + al((size_t)T * D * 2));
+  __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(qkv) + al((size_t)T * 3 * D * 2));
+  __nv_bfloat16* m = reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(o) + al((size_t)T * D * 2));
+  float* xt = reinterpret_cast<float*>(reinterpret_cast<char*>(m) + al((size_t)T * F * 2));
+  float* xsp = xt + T * D;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int launches_before = 0;
+  (void)launches_before;
+  int total = 0;
+  auto count = [&]() { total += h->launches; h->launches = 0; };
+  const long long D3 = 3LL * D;
+  // views of q / k / v inside the QKV output [K, N, 3D] (head h at columns h d of each third)
+  const View qt{K, H, N, (long long)N * D3, (long long)d, D3};            // temporal: axis t, groups (h, n)
+  const View qs{N, H, K, D3, (long long)d, (long long)N * D3};            // spatial: axis n, groups (h, t)
+  const View ot = temporal_view(K, N, H, d), os = spatial_view(K, N, H, d);
+  // ---- temporal stage ----
+  if ((s = layer_norm(h, st, reinterpret_cast<const __nv_bfloat16*>(x), w->ln_t_g, w->ln_t_b, hb, T, D)) != TSF_OK) return s;
+  count();
+  if ((s = gemm(h, st, GEPI_BIAS_BF16, hb, w->w_qkv_t, w->b_qkv_t, nullptr, qkv, T, 3 * D, D)) != TSF_OK) return s;
+  count();
+  {
+    StageTimer tm(h, st, 0);
+    s = run_attention(h, qt, qkv, qkv + D, qkv + 2 * D, EPI_OUT16, o, nullptr, st, &ot);
+    tm.done();
+    if (s != TSF_OK) return s;
+    count();
+  }
+  if ((s = gemm(h, st, GEPI_RESB_F32, o, w->w_o_t, w->b_o_t, x, xt, T, D, D)) != TSF_OK) return s;
+  count();
+  // ---- spatial stage ----
+  if ((s = layer_norm(h, st, xt, w->ln_s_g, w->ln_s_b, hb, T, D)) != TSF_OK) return s;
+  count();
+  if ((s = gemm(h, st, GEPI_BIAS_BF16, hb, w->w_qkv_s, w->b_qkv_s, nullptr, qkv, T, 3 * D, D)) != TSF_OK) return s;
+  count();
+  {
+    StageTimer tm(h, st, 1);
+    s = run_attention(h, qs, qkv, qkv + D, qkv + 2 * D, EPI_OUT16, o, nullptr, st, &os);
+    tm.done();
+    if (s != TSF_OK) return s;
+    count();
+  }
+  if ((s = gemm(h, st, GEPI_RES_F32, o, w->w_o_s, w->b_o_s, xt, xsp, T, D, D)) != TSF_OK) return s;
+  count();
+  // ---- MLP ----
+  if ((s = layer_norm(h, st, xsp, w->ln_m_g, w->ln_m_b, hb, T, D)) != TSF_OK) return s;
+  count();
+  if ((s = gemm(h, st, GEPI_GELU_BF16, hb, w->w_1, w->b_1, nullptr, m, T, F, D)) != TSF_OK) return s;
+  count();
+  if ((s = gemm(h, st, GEPI_RES_F32, m, w->w_2, w->b_2, xsp, y, T, D, F)) != TSF_OK) return s;
+  count();
+  h->launches = total;
+  return TSF_OK;
 }
 
 // ---------------------------------------------------------------------------

@@ -20,4 +20,7 @@ from .fields import (  # noqa: F401
     bf16_bits_to_f64,
     f64_to_bf16_bits,
     bits_to_torch,
+    make_block_params,
+    block_params_f64,
+    BLOCK_PARAM_SHAPES,
 )

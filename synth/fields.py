@@ -220,3 +220,47 @@ def make_qkv(K, N, H, d, seed=0, kind="field", peaky=False, frames=None, tokens=
 def make_x(K, N, H, d, seed=0, kind="field", frames=None, tokens=None):
     """The single block input x (q = k = v = x per stage, reading G1)."""
     return _make(kind, K, N, H, d, seed, "x", frames, tokens, 1.0)
+
+
+# ---------------------------------------------------------------------------
+# random parameters of the full divided block (NEXT-1): draws only
+# ---------------------------------------------------------------------------
+
+BLOCK_PARAM_SHAPES = {  # name -> (shape as a function of D = H d and F, kind)
+    "ln_t_g": ("D", "gain"), "ln_t_b": ("D", "bias"),
+    "w_qkv_t": ("3D,D", "weight"), "b_qkv_t": ("3D", "bias"),
+    "w_o_t": ("D,D", "weight"), "b_o_t": ("D", "bias"),
+    "ln_s_g": ("D", "gain"), "ln_s_b": ("D", "bias"),
+    "w_qkv_s": ("3D,D", "weight"), "b_qkv_s": ("3D", "bias"),
+    "w_o_s": ("D,D", "weight"), "b_o_s": ("D", "bias"),
+    "ln_m_g": ("D", "gain"), "ln_m_b": ("D", "bias"),
+    "w_1": ("F,D", "weight"), "b_1": ("F", "bias"),
+    "w_2": ("D,F", "weight"), "b_2": ("D", "bias"),
+}
+
+
+def make_block_params(H: int, d: int, F: int, seed: int = 7) -> dict:
+    """Random-init parameters of one divided block (there are no trained weights).
+
+    Weights [out, in] ~ N(0, 1/in) rounded to bf16 (returned as uint16 bits);
+    LayerNorm gains 1 + N(0, 0.1^2), biases N(0, 0.1^2), both rounded to fp32
+    (returned as float32).  Keyed by (seed, parameter index).
+    """
+    D = H * d
+    dims = {"D": D, "3D": 3 * D, "F": F}
+    out = {}
+    for i, (name, (shp, kind)) in enumerate(BLOCK_PARAM_SHAPES.items()):
+        shape = tuple(dims[s] for s in shp.split(","))
+        g = _rng(seed, 50 + i)
+        if kind == "weight":
+            out[name] = f64_to_bf16_bits(g.normal(0.0, 1.0 / math.sqrt(shape[1]), shape))
+        elif kind == "gain":
+            out[name] = (1.0 + g.normal(0.0, 0.1, shape)).astype(np.float32)
+        else:
+            out[name] = g.normal(0.0, 0.1, shape).astype(np.float32)
+    return out
+
+
+def block_params_f64(params: dict) -> dict:
+    """The exact float64 values of make_block_params' bf16 / fp32 parameters."""
+    return {k: (bf16_bits_to_f64(v) if v.dtype == np.uint16 else v.astype(np.float64)) for k, v in params.items()}

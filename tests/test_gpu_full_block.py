@@ -1,0 +1,68 @@
+"""The full TimeSformer divided block on the GPU (reading
+G21): pre-LN, QKV / output projections and MLP (tcgen05 GEMMs with fused
+bias / GELU / residual epilogues, LayerNorm kernel) around the factorized
+attention of PAPER.md P:64, against the fp64 oracle (oracle.full_block) on the
+same bf16 inputs and bf16 / fp32 parameters.
+
+Tolerance (G21): the GPU rounds five intermediates to bf16 (LN
+outputs, q/k/v, attention outputs, GELU output; 2^-9 relative each) where the
+oracle keeps fp64; with unit-variance branches that gives ~1e-2 absolute
+error per branch on |y| ~ 10.  Gate: rel-L2 <= 1e-2 (the north-star relative
+gate) and max-abs <= 5e-2.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def dev_params(params):
+    out = {}
+    for k, v in params.items():
+        if v.dtype == np.uint16:
+            out[k] = synth.bits_to_torch(v, "cuda")
+        else:
+            out[k] = torch.from_numpy(v).cuda()
+    return out
+
+
+@pytest.mark.parametrize("shape,F", [((4, 300, 2, 64), 512), ((8, 256, 4, 32), 256), ((3, 130, 1, 128), 384),
+                                     ((200, 3, 2, 64), 256), ((8, 1024, 8, 64), 2048)])
+def test_full_block_matches_oracle(tsf_lib, shape, F):
+    K, N, H, d = shape
+    xb = synth.make_x(K, N, H, d, seed=51)
+    params = synth.make_block_params(H, d, F, seed=52)
+    layer = tsf_lib.Layer(K, N, H, d)
+    y = layer.full_block(synth.bits_to_torch(xb, "cuda"), dev_params(params))
+    torch.cuda.synchronize()
+    got = y.double().cpu().numpy()
+    want = oracle.full_block(synth.bf16_bits_to_f64(xb), synth.block_params_f64(params))
+    err = np.abs(got - want).max()
+    rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+    print(f"full block {shape} F={F}: max-abs {err:.3e} rel-L2 {rel:.3e} max|ref| {np.abs(want).max():.2f}")
+    assert np.all(np.isfinite(got)) and rel <= 1e-2 and err <= 5e-2
+
+
+def test_full_block_zero_output_projections_is_identity(tsf_lib):
+    """W_o / b_o of both stages and W_2 / b_2 zero: y = x exactly (fp32 residual stream)."""
+    K, N, H, d = 4, 200, 2, 64
+    xb = synth.make_x(K, N, H, d, seed=53)
+    params = synth.make_block_params(H, d, 256, seed=54)
+    for k in ("w_o_t", "b_o_t", "w_o_s", "b_o_s", "w_2", "b_2"):
+        params[k] = np.zeros_like(params[k])
+    layer = tsf_lib.Layer(K, N, H, d)
+    y = layer.full_block(synth.bits_to_torch(xb, "cuda"), dev_params(params))
+    torch.cuda.synchronize()
+    assert torch.equal(y.cpu(), synth.bits_to_torch(xb).float())
+
+
+def test_full_block_rejects_unsupported_width(tsf_lib):
+    layer = tsf_lib.Layer(2, 64, 1, 32)                  # D = 32: not a multiple of 128
+    params = dev_params(synth.make_block_params(1, 32, 128))
+    with pytest.raises(tsf_lib.TsfError) as e:
+        layer.full_block(torch.zeros((2, 64, 1, 32), dtype=torch.bfloat16, device="cuda"), params)
+    assert e.value.status == tsf_lib.TSF_ERR_UNSUPPORTED

@@ -383,3 +383,77 @@ def test_storm_special_cases():
     perm = np.random.default_rng(3).permutation(M)
     np.testing.assert_allclose(oracle.storm_attention(u, ctx[:, perm], 1.5, 1.0),
                                oracle.storm_attention(u, ctx, 1.5, 1.0), rtol=0, atol=1e-12)
+
+
+# --- full divided block (NEXT-1, reading G21) -------------------------------
+
+def _torch_full_block(x, p):
+    """The same block composed from torch library modules in fp64 (layer_norm,
+    linear, SDPA per group, exact GELU): an implementation independent of the
+    oracle's numpy arithmetic."""
+    import torch.nn.functional as F
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a))
+    K, N, H, d = x.shape
+    D = H * d
+    P = {k: t(v) for k, v in p.items()}
+    X = t(x).reshape(K, N, D)
+
+    def proj(h, w, b):
+        z = F.linear(h, w, b)
+        return [z[..., i * D:(i + 1) * D].reshape(K, N, H, d) for i in range(3)]
+
+    def attn(q, k, v, axis):      # axis 0: over frames (temporal), 1: over tokens (spatial)
+        perm = (1, 2, 0, 3) if axis == 0 else (0, 2, 1, 3)
+        inv = (2, 0, 1, 3) if axis == 0 else (0, 2, 1, 3)
+        o = F.scaled_dot_product_attention(q.permute(*perm), k.permute(*perm), v.permute(*perm))
+        return o.permute(*inv).reshape(K, N, D)
+
+    q, k, v = proj(F.layer_norm(X, (D,), P["ln_t_g"], P["ln_t_b"], 1e-5), P["w_qkv_t"], P["b_qkv_t"])
+    Xt = X + F.linear(attn(q, k, v, 0), P["w_o_t"], P["b_o_t"])
+    q, k, v = proj(F.layer_norm(Xt, (D,), P["ln_s_g"], P["ln_s_b"], 1e-5), P["w_qkv_s"], P["b_qkv_s"])
+    Xs = Xt + F.linear(attn(q, k, v, 1), P["w_o_s"], P["b_o_s"])
+    m = F.gelu(F.linear(F.layer_norm(Xs, (D,), P["ln_m_g"], P["ln_m_b"], 1e-5), P["w_1"], P["b_1"]))
+    return (Xs + F.linear(m, P["w_2"], P["b_2"])).reshape(K, N, H, d).numpy()
+
+
+def _params(H, d, F, seed=7):
+    import synth
+    return synth.block_params_f64(synth.make_block_params(H, d, F, seed))
+
+
+@pytest.mark.parametrize("shape", [(3, 5, 2, 4), (1, 6, 1, 8), (4, 1, 2, 4)])
+def test_full_block_matches_torch_library_composition(shape):
+    K, N, H, d = shape
+    x = rand(*shape)
+    p = _params(H, d, 4 * H * d)
+    np.testing.assert_allclose(oracle.full_block(x, p), _torch_full_block(x, p), rtol=0, atol=1e-11)
+
+
+def test_full_block_zero_output_projections_is_identity():
+    """W_o, b_o of both stages and W_2, b_2 zero: every branch adds exactly zero."""
+    K, N, H, d = 3, 4, 2, 4
+    p = _params(H, d, 32)
+    for k in ("w_o_t", "b_o_t", "w_o_s", "b_o_s", "w_2", "b_2"):
+        p[k] = np.zeros_like(p[k])
+    x = rand(K, N, H, d)
+    np.testing.assert_array_equal(oracle.full_block(x, p), x)
+
+
+def test_full_block_permutation_equivariance():
+    K, N, H, d = 3, 5, 2, 4
+    p = _params(H, d, 32)
+    x = rand(K, N, H, d)
+    y = oracle.full_block(x, p)
+    pn, pk = np.random.default_rng(5).permutation(N), np.random.default_rng(6).permutation(K)
+    np.testing.assert_allclose(oracle.full_block(x[:, pn], p), y[:, pn], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(oracle.full_block(x[pk], p), y[pk], rtol=0, atol=1e-12)
+
+
+def test_layer_norm_and_gelu_closed_forms():
+    x = np.array([[1.0, 2.0, 3.0, 6.0]])
+    # mean 3, biased variance 3.5
+    want = (x - 3.0) / math.sqrt(3.5 + 1e-5)
+    np.testing.assert_allclose(oracle.layer_norm(x, np.ones(4), np.zeros(4)), want, rtol=0, atol=1e-15)
+    assert oracle.gelu(np.array([0.0]))[0] == 0.0
+    # GELU(1) = 0.5 (1 + erf(1/sqrt 2)) = Phi(1) = 0.8413447460685429 (standard normal CDF)
+    assert abs(oracle.gelu(np.array([1.0]))[0] - 0.8413447460685429) < 1e-15

@@ -1,5 +1,5 @@
 O=gpurun_out/r2e; mkdir -p $O
-timeout 900 python -m pytest -x -q -rA tests/test_gpu_storm.py tests/test_gpu_joint.py tests/test_gpu_dist_sim.py tests/test_gpu_parity.py -k "storm or joint or block_matches or C2_block_every_row and 0 or nonfinite or sim_block or deterministic or temporal_and_spatial" > $O/pytest.log 2>&1; echo pytest rc=$?; tail -2 $O/pytest.log
+timeout 900 python -m pytest -q -rA tests/test_gpu_full_block.py tests/test_gpu_storm.py tests/test_gpu_joint.py tests/test_gpu_dist_sim.py tests/test_gpu_parity.py -k "full_block or storm or joint or block_matches or C2_block_every_row and 0 or nonfinite or sim_block or deterministic or temporal_and_spatial" > $O/pytest.log 2>&1; echo pytest rc=$?; tail -2 $O/pytest.log
 TSF_LIB=paper_2604_16590_b200/libtsf_trace.so timeout 120 python tools/trace_stream.py > $O/trace_stream.txt 2>&1; tail -1 $O/trace_stream.txt
 for fl in 0 2; do for emu in 4 6 8; do
   echo "== flags=$fl emu=$emu"
