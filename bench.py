@@ -161,10 +161,17 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(K, N, H, d, world),
+            "data": "synthetic", "config": dict(workload_config(K, N, H, d, world), l2_sets=l2_sets(K, N, H, d, world)),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def l2_sets(K, N, H, d, world):
+    """Rotating input/output sets so a step never finds its data in L2 (each set
+    is one rank's bf16 x token shard + fp32 y frame shard; R sets > 3x L2)."""
+    set_bytes = K * (N // world) * H * d * 2 + (K // world) * N * H * d * 4
+    return max(2, -(-3 * L2_BYTES // set_bytes))
 
 
 def workload_config(K, N, H, d, world, cfg="C2"):
@@ -223,8 +230,7 @@ def main():
     else:  # large shapes: seeded device-side iid inputs (generation is not timed)
         g = torch.Generator(device="cuda").manual_seed(1000 + rank)
         x0 = torch.randn((K, Nl, H, d), generator=g, device="cuda").clamp_(-4, 4).to(torch.bfloat16)
-    set_bytes = x0.numel() * 2 + Kl * N * H * d * 4
-    R = max(2, int(np.ceil(3 * L2_BYTES / set_bytes)))
+    R = l2_sets(K, N, H, d, world)
     xs = [x0] + [x0.clone() for _ in range(R - 1)]
     ys = [torch.empty(layer.frame_shard_shape, dtype=torch.float32, device="cuda") for _ in range(R)]
     stream = torch.cuda.current_stream()
@@ -285,11 +291,30 @@ def main():
     barrier()
     e2e_s = time.perf_counter() - t0
 
+    # the same temporal kernel writing locally (no exchange): a single-GPU handle of
+    # this rank's token-shard shape, timed on its own (fused-exchange bandwidth)
+    tl_ms = 0.0
+    if world > 1 and layer.exchange_mode() == 2:
+        loc = tsf.Layer(K, Nl, H, d)
+        yl = torch.empty((K, Nl, H, d), dtype=torch.float32, device="cuda")
+        for i in range(3):
+            loc.block(xs[i % R], out=yl)
+        torch.cuda.synchronize()
+        loc.set_timing(True)
+        reps = max(20, min(args.steps, 200))
+        for i in range(reps):
+            loc.block(xs[i % R], out=yl)
+        torch.cuda.synchronize()
+        tl_ms = loc.stage_ms(tsf.STAGE_TEMPORAL)[0] / reps
+        loc.close()
+        del yl
+
     # max over ranks
-    vals = torch.tensor([ms, e2e_s, st_ms[1][0], st_ms[0][0], st_ms[2][0]], dtype=torch.float64, device="cuda")
+    vals = torch.tensor([ms, e2e_s, st_ms[1][0], st_ms[0][0], st_ms[2][0], tl_ms], dtype=torch.float64,
+                        device="cuda")
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    ms, e2e_s, sp_ms, tp_ms, rs_ms = vals.tolist()
+    ms, e2e_s, sp_ms, tp_ms, rs_ms, tl_ms = vals.tolist()
 
     if rank == 0:
         pk = peaks()
@@ -309,7 +334,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": scaling,
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "vs_baseline": None, "dtype": "bf16 in; fp16 X_t, MMA operands and P; fp32 accumulate and y",
+            "data": "synthetic",
             "config": dict(workload_config(K, N, H, d, world, args.config), l2_sets=R),
             "tflops": F / (step_ms / 1e3) / 1e12,
             "tflops_frac_of_measured": F / (step_ms / 1e3) / 1e12 / (pk["tflops"] * world),
@@ -336,6 +362,16 @@ def main():
                 line["a2a"]["mode"] = ("fused: the temporal kernel stores X_t rows into each rank's frame shard "
                                        "over NVLink (CUDA IPC); the exchange stage is only the 1-int NCCL "
                                        "all-reduce that orders the stores")
+                # exchange bandwidth: the bytes each rank sends to peers over the extra time
+                # its temporal stage takes against the same kernel writing locally (P = 1
+                # handle of the rank's token-shard shape), max over ranks
+                dt_ms = tp_ms / args.steps - tl_ms
+                line["a2a"].update(temporal_ms_local_same_shape=tl_ms, temporal_ms_with_exchange=tp_ms / args.steps,
+                                   exchange_extra_ms=dt_ms,
+                                   exchange_GBs_per_rank=(a2a_bytes * (world - 1) / world / (dt_ms / 1e3) / 1e9
+                                                          if dt_ms > 0 else None),
+                                   exchange_GBs_frac_of_nvlink=(a2a_bytes * (world - 1) / world / (dt_ms / 1e3) / 1e9
+                                                                / 900 if dt_ms > 0 else None))
             else:
                 algbw = a2a_bytes / (rs_step_ms / 1e3) / 1e9
                 line["a2a"].update(mode="NCCL grouped send/recv per head chunk; exchange(c+1) overlaps spatial(c)",

@@ -64,6 +64,15 @@ TSF_DEV void ffma2(float& x0, float& x1, float a0, float a1, float b0, float b1,
       : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
 }
 
+// Packed fp32x2 add (FADD2): (a0, a1) += (b0, b1)
+TSF_DEV void add2(float& a0, float& a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 ra, rb;\n\t"
+      "mov.b64 ra, {%0, %1};\n\tmov.b64 rb, {%2, %3};\n\t"
+      "add.rn.ftz.f32x2 ra, ra, rb;\n\tmov.b64 {%0, %1}, ra;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(b0), "f"(b1));
+}
+
 // 2^x for a pair on the FMA/ALU pipes (no MUFU), x <= 0: Cody-Waite split
 // x = i + f, f in [0, 1), 2^f by a degree-3 polynomial with p(0) = 1 (minimax
 // in relative error, max 8.6e-5: below the 2^-9 / 2^-12 rounding that P gets

@@ -20,6 +20,7 @@
 #include "attn_flash.cuh"
 #include "attn_packed.cuh"
 #include "attn_stream.cuh"
+#include "attn_flash3.cuh"
 #include "gemm.cuh"
 #include "layout.cuh"
 
@@ -396,6 +397,51 @@ static tsf_status dispatch_d(tsf_handle* h, bool packed, int win, int epi, cudaS
 
 // Attention over one view: q/k/v (q == k == v for the block stages).  The
 // output (o or y) uses the strides of `ov` (default: the input view's).
+// One-query-tile-per-CTA flash kernel, three CTAs per SM (attn_flash3.cuh):
+// d = 64, spatial block stage and the standalone calls.  TSF_FLASH3=0 selects
+// the two-tile kernel (attn_flash.cuh) for A/B measurements.
+static bool use_flash3(int d, int epi) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("TSF_FLASH3");
+    env = e ? atoi(e) : 1;
+  }
+  return env != 0 && d == 64 && (epi == EPI_BLOCK_S || epi == EPI_OUT16);
+}
+static int flash3_emu() {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("TSF_EMU3");
+    env = e ? atoi(e) : 4;
+  }
+  return env;
+}
+
+template <int EPI, int EMU>
+static tsf_status launch_flash3_emu(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
+                                    const CUtensorMap& mv, const AttnParams& p) {
+  constexpr int NST = EpiTraits<EPI>::SHARED ? 6 : 4;
+  using C = Flash3Cfg<64, EPI, NST>;
+  const long long items = (long long)p.n_qpairs * p.A * p.B;
+  if (items > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "too many work items");
+  AttnParams pp = p;
+  pp.num_items = (int)items;
+  const long long cap = 3LL * h->num_sms;
+  return launch(h, attn_flash3_kernel<64, EPI, NST, EMU>, (int)(items < cap ? items : cap), C::THREADS, C::SMEM, st,
+                pp, mq, mk, mv);
+}
+
+template <int EPI>
+static tsf_status launch_flash3(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
+                                const CUtensorMap& mv, const AttnParams& p) {
+  switch (flash3_emu()) {
+    case 0: return launch_flash3_emu<EPI, 0>(h, st, mq, mk, mv, p);
+    case 2: return launch_flash3_emu<EPI, 2>(h, st, mq, mk, mv, p);
+    case 6: return launch_flash3_emu<EPI, 6>(h, st, mq, mk, mv, p);
+    default: return launch_flash3_emu<EPI, 4>(h, st, mq, mk, mv, p);
+  }
+}
+
 // Flash kernel with fixed tile / exp settings for the secondary calls: joint
 // attention with a block or causal mask (tsf_joint_attn, MASK = 1) and the
 // STORM epilogues (tsf_storm_attn), bf16 operands and P.
@@ -502,12 +548,15 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
       h->use_pm = true;
     }
   } else {
-    p.n_qpairs = (v.L + 255) / 256;
-    const int sub = special ? ((d == 64) ? 96 : 128) : flash_sub(d);  // K/V tile rows
+    const bool f3 = !special && use_flash3(d, epi);
+    p.n_qpairs = f3 ? (v.L + 127) / 128 : (v.L + 255) / 256;   // flash3: 128-row query tiles
+    const int sub = f3 ? 64 : special ? ((d == 64) ? 96 : 128) : flash_sub(d);  // K/V tile rows
     p.nkv = (kvv->L + sub - 1) / sub;
     if ((s = make_map(h, &mq, q, d, v, 128, 1, 1, f16)) != TSF_OK) return s;
     if ((s = make_map(h, &mk, k, d, *kvv, sub, 1, 1, f16)) != TSF_OK) return s;
     if ((s = make_map(h, &mv, vv, d, *kvv, sub, 1, 1, f16)) != TSF_OK) return s;
+    if (f3) return epi == EPI_BLOCK_S ? launch_flash3<EPI_BLOCK_S>(h, st, mq, mk, mv, p)
+                                      : launch_flash3<EPI_OUT16>(h, st, mq, mk, mv, p);
     if (special) {
       switch (d) {
         case 32: return launch_flash_special<32>(h, epi, mask, st, mq, mk, mv, p);
