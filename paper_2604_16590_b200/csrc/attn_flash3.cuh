@@ -48,8 +48,8 @@ struct Flash3Cfg {
   static constexpr uint32_t COL_O = 0, COL_S = D;          // 128 TMEM columns
 };
 
-template <int D, int EPI, int NST, int EMU>
-__global__ void __launch_bounds__(192, 3)
+template <int D, int EPI, int NST, int EMU, int CPS>
+__global__ void __launch_bounds__(192, CPS)
 attn_flash3_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                    const __grid_constant__ CUtensorMap tv, const AttnParams p) {
   using C = Flash3Cfg<D, EPI, NST>;
@@ -149,7 +149,8 @@ attn_flash3_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
                    make_sdesc(ka + 32 * kk, 16, 8 * C::SWB, SWZ_128B), idesc_qk, kk > 0);
           mma_commit(s_full);
           if (j == nkv - 1) mma_commit(q_empty);  // Q read by every QK^T of the item
-          mbar_wait_sleep(p_full, G & 1);
+          mbar_wait(p_full, G & 1);             // critical path: spin, do not sleep
+          TSF_STAMP(p, 5, 2 * (j & 511));
           tc_fence_after();
           if (j == 0 && k > 0) {                 // the epilogue of the previous item has read O
             mbar_wait_sleep(o_empty, (k - 1) & 1);
@@ -163,6 +164,7 @@ attn_flash3_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
                    (j > 0 || kk > 0) ? 1u : 0u);
           mma_commit(&kv_empty[s]);
           if (j == nkv - 1) mma_commit(o_full);
+          TSF_STAMP(p, 5, 2 * (j & 511) + 1);
         }
       }
     }
@@ -181,6 +183,7 @@ attn_flash3_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
       float l0 = 0.f, l1 = 0.f;
       for (int j = 0; j < nkv; ++j, ++G) {
         mbar_wait(s_full, G & 1);
+        TSF_STAMP(p, warp, 4 * (j & 255));
         tc_fence_after();
         const int valid = Lk - j * SUB;          // keys >= valid are beyond the sequence (-inf)
         // pass 1: the row max over the 64 scores (two 32-column halves)
@@ -224,13 +227,16 @@ attn_flash3_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
           }
         }
         const float nmb = -m_run;
+        TSF_STAMP(p, warp, 4 * (j & 255) + 1);
         // pass 2: 16-column chunks reloaded from TMEM: scale, exponentiate, pack,
         // store P over S (P of keys c0.. lands in columns c0/2.., below the next chunk)
+        uint32_t sb[2][16];                      // chunk c0 + 16 loads while chunk c0 computes
+        tmem_ld_x16(tSrow, sb[0]);
+        tmem_wait_ld();
 #pragma unroll
         for (int c0 = 0; c0 < SUB; c0 += 16) {
-          uint32_t sv[16];
-          tmem_ld_x16(tSrow + c0, sv);
-          tmem_wait_ld();
+          uint32_t* sv = sb[(c0 / 16) & 1];
+          if (c0 + 16 < SUB) tmem_ld_x16(tSrow + c0 + 16, sb[((c0 / 16) + 1) & 1]);
           if (valid < SUB) {
 #pragma unroll
             for (int c = 0; c < 16; ++c) sv[c] = (c0 + c < valid) ? sv[c] : 0xFF800000u;
@@ -255,11 +261,13 @@ attn_flash3_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant
             add2(l0, l1, pv[c], pv[c + 1]);
           }
           tmem_st_x8(tSrow + c0 / 2, pk);
+          if (c0 + 16 < SUB) tmem_wait_ld();
         }
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
+        TSF_STAMP(p, warp, 4 * (j & 255) + 2);
       }
       // ---- epilogue of item k, in two 32-column halves ----
       mbar_wait(o_full, k & 1);

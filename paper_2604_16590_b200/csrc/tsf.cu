@@ -404,7 +404,7 @@ static bool use_flash3(int d, int epi) {
   static int env = -2;
   if (env == -2) {
     const char* e = getenv("TSF_FLASH3");
-    env = e ? atoi(e) : 1;
+    env = e ? atoi(e) : 0;
   }
   return env != 0 && d == 64 && (epi == EPI_BLOCK_S || epi == EPI_OUT16);
 }
@@ -417,18 +417,35 @@ static int flash3_emu() {
   return env;
 }
 
-template <int EPI, int EMU>
-static tsf_status launch_flash3_emu(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
+static int flash3_cps() {  // CTAs per SM (TSF_F3CTAS: 3 | 4)
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("TSF_F3CTAS");
+    env = e ? atoi(e) : 3;
+  }
+  return env == 4 ? 4 : 3;
+}
+
+template <int EPI, int EMU, int CPS>
+static tsf_status launch_flash3_cps(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
                                     const CUtensorMap& mv, const AttnParams& p) {
-  constexpr int NST = EpiTraits<EPI>::SHARED ? 6 : 4;
+  constexpr bool SH = EpiTraits<EPI>::SHARED;
+  constexpr int NST = CPS == 4 ? (SH ? 3 : 2) : (SH ? 6 : 4);
   using C = Flash3Cfg<64, EPI, NST>;
   const long long items = (long long)p.n_qpairs * p.A * p.B;
   if (items > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "too many work items");
   AttnParams pp = p;
   pp.num_items = (int)items;
-  const long long cap = 3LL * h->num_sms;
-  return launch(h, attn_flash3_kernel<64, EPI, NST, EMU>, (int)(items < cap ? items : cap), C::THREADS, C::SMEM, st,
-                pp, mq, mk, mv);
+  const long long cap = (long long)CPS * h->num_sms;
+  return launch(h, attn_flash3_kernel<64, EPI, NST, EMU, CPS>, (int)(items < cap ? items : cap), C::THREADS, C::SMEM,
+                st, pp, mq, mk, mv);
+}
+
+template <int EPI, int EMU>
+static tsf_status launch_flash3_emu(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
+                                    const CUtensorMap& mv, const AttnParams& p) {
+  if (flash3_cps() == 4) return launch_flash3_cps<EPI, EMU, 4>(h, st, mq, mk, mv, p);
+  return launch_flash3_cps<EPI, EMU, 3>(h, st, mq, mk, mv, p);
 }
 
 template <int EPI>
@@ -436,7 +453,6 @@ static tsf_status launch_flash3(tsf_handle* h, cudaStream_t st, const CUtensorMa
                                 const CUtensorMap& mv, const AttnParams& p) {
   switch (flash3_emu()) {
     case 0: return launch_flash3_emu<EPI, 0>(h, st, mq, mk, mv, p);
-    case 2: return launch_flash3_emu<EPI, 2>(h, st, mq, mk, mv, p);
     case 6: return launch_flash3_emu<EPI, 6>(h, st, mq, mk, mv, p);
     default: return launch_flash3_emu<EPI, 4>(h, st, mq, mk, mv, p);
   }
