@@ -36,6 +36,10 @@ from .attention import (  # noqa: F401
     linear,
     gelu,
     full_block,
+    attend_bwd,
+    temporal_bwd,
+    spatial_bwd,
+    block_bwd,
     temporal_rows,
     spatial_rows,
     block_rows,

@@ -383,3 +383,64 @@ def full_block(x: np.ndarray, p: dict) -> np.ndarray:
     m = gelu(linear(layer_norm(xsp, p["ln_m_g"], p["ln_m_b"]), p["w_1"], p["b_1"]))
     y = xsp + linear(m, p["w_2"], p["b_2"])
     return y.reshape(K, N, H, d)
+
+
+# ---------------------------------------------------------------------------
+# backward pass: gradients of the attention stages and of
+# the block, from the definitions (P:64 forward; training)
+# ---------------------------------------------------------------------------
+
+def attend_bwd(Q: np.ndarray, Kt: np.ndarray, V: np.ndarray, dO: np.ndarray):
+    """Gradients of O = softmax(Q Kt^T / sqrt d) V for groups on the leading axes:
+
+        P = softmax_rows(S), dV = P^T dO, dP = dO V^T,
+        dS = P * (dP - rowsum(dP * P)),  dQ = dS Kt / sqrt d,  dK = dS^T Q / sqrt d.
+    """
+    d = Q.shape[-1]
+    s = 1.0 / math.sqrt(d)
+    S = np.matmul(Q, np.swapaxes(Kt, -1, -2)) * s
+    P = softmax_rows(S)
+    dV = np.matmul(np.swapaxes(P, -1, -2), dO)
+    dP = np.matmul(dO, np.swapaxes(V, -1, -2))
+    dS = P * (dP - np.sum(dP * P, axis=-1, keepdims=True))
+    dQ = np.matmul(dS, Kt) * s
+    dK = np.matmul(np.swapaxes(dS, -1, -2), Q) * s
+    return dQ, dK, dV
+
+
+def _stage_bwd(q, k, v, do, axis):
+    """Gradients of the temporal (axis 0) or spatial (axis 1) stage, [K, N, H, d]."""
+    _check(q, k, v, do)
+    K, N, H, d = q.shape
+    if axis == 0:
+        g = lambda a: a.transpose(1, 2, 0, 3).reshape(N * H, K, d)
+        ug = lambda a: a.reshape(N, H, K, d).transpose(2, 0, 1, 3)
+    else:
+        g = lambda a: a.transpose(0, 2, 1, 3).reshape(K * H, N, d)
+        ug = lambda a: a.reshape(K, H, N, d).transpose(0, 2, 1, 3)
+    dq, dk, dv = attend_bwd(g(q), g(k), g(v), g(do))
+    return ug(dq).copy(), ug(dk).copy(), ug(dv).copy()
+
+
+def temporal_bwd(q, k, v, do):
+    """(dq, dk, dv) of temporal(q, k, v) for the output gradient do."""
+    return _stage_bwd(q, k, v, do, 0)
+
+
+def spatial_bwd(q, k, v, do):
+    """(dq, dk, dv) of spatial(q, k, v) for the output gradient do."""
+    return _stage_bwd(q, k, v, do, 1)
+
+
+def block_bwd(x: np.ndarray, dy: np.ndarray) -> np.ndarray:
+    """dx of block(x) = X_t + S(X_t, X_t, X_t), X_t = x + T(x, x, x), for dy:
+
+        dX_t = dy + (dq + dk + dv of S at X_t),  dx = dX_t + (dq + dk + dv of T at x)
+    (q = k = v = the stage input, so its gradient is the sum of the three).
+    """
+    _check(x, dy)
+    xt = x + temporal(x, x, x)
+    a, b, c = spatial_bwd(xt, xt, xt, dy)
+    dxt = dy + a + b + c
+    a, b, c = temporal_bwd(x, x, x, dxt)
+    return dxt + a + b + c

@@ -457,3 +457,61 @@ def test_layer_norm_and_gelu_closed_forms():
     assert oracle.gelu(np.array([0.0]))[0] == 0.0
     # GELU(1) = 0.5 (1 + erf(1/sqrt 2)) = Phi(1) = 0.8413447460685429 (standard normal CDF)
     assert abs(oracle.gelu(np.array([1.0]))[0] - 0.8413447460685429) < 1e-15
+
+
+# --- backward (NEXT-2) -------------------------------------------------------
+
+def _autograd_stage(q, k, v, do, axis):
+    """torch autograd through SDPA in fp64 (library routine)."""
+    K, N, H, d = q.shape
+    perm = (1, 2, 0, 3) if axis == 0 else (0, 2, 1, 3)
+    inv = (2, 0, 1, 3) if axis == 0 else (0, 2, 1, 3)
+    ts = [torch.from_numpy(np.ascontiguousarray(a)).requires_grad_(True) for a in (q, k, v)]
+    o = torch.nn.functional.scaled_dot_product_attention(*(t.permute(*perm) for t in ts)).permute(*inv)
+    o.backward(torch.from_numpy(do))
+    return [t.grad.numpy() for t in ts]
+
+
+@pytest.mark.parametrize("axis", [0, 1])
+@pytest.mark.parametrize("shape", [(5, 6, 2, 4), (1, 7, 1, 8), (3, 1, 2, 4)])
+def test_stage_bwd_matches_library_autograd(axis, shape):
+    q, k, v, do = (rand(*shape) for _ in range(4))
+    got = (oracle.temporal_bwd if axis == 0 else oracle.spatial_bwd)(q, k, v, do)
+    for g, w in zip(got, _autograd_stage(q, k, v, do, axis)):
+        np.testing.assert_allclose(g, w, rtol=0, atol=1e-11)
+
+
+def test_block_bwd_matches_finite_differences():
+    """Central differences of <dy, block(x)> in fp64 (independent of any autograd)."""
+    K, N, H, d = 3, 4, 1, 3
+    x, dy = rand(K, N, H, d), rand(K, N, H, d)
+    dx = oracle.block_bwd(x, dy)
+    f = lambda a: float(np.sum(dy * oracle.block(a)))
+    h = 1e-6
+    num = np.zeros_like(x)
+    for idx in np.ndindex(*x.shape):
+        e = np.zeros_like(x)
+        e[idx] = h
+        num[idx] = (f(x + e) - f(x - e)) / (2 * h)
+    np.testing.assert_allclose(dx, num, rtol=0, atol=1e-7)
+
+
+def test_block_bwd_matches_library_autograd():
+    K, N, H, d = 4, 5, 2, 4
+    x, dy = rand(K, N, H, d), rand(K, N, H, d)
+    xt_ = torch.from_numpy(x).requires_grad_(True)
+    sdpa = torch.nn.functional.scaled_dot_product_attention
+    t = lambda a: sdpa(a.permute(1, 2, 0, 3), a.permute(1, 2, 0, 3), a.permute(1, 2, 0, 3)).permute(2, 0, 1, 3)
+    s_ = lambda a: sdpa(a.permute(0, 2, 1, 3), a.permute(0, 2, 1, 3), a.permute(0, 2, 1, 3)).permute(0, 2, 1, 3)
+    Xt = xt_ + t(xt_)
+    y = Xt + s_(Xt)
+    y.backward(torch.from_numpy(dy))
+    np.testing.assert_allclose(oracle.block_bwd(x, dy), xt_.grad.numpy(), rtol=0, atol=1e-11)
+
+
+def test_stage_bwd_closed_forms():
+    """K = 1: temporal output = v, so dv = do and dq = dk = 0 exactly (one key, weight 1)."""
+    q, k, v, do = (rand(1, 5, 2, 4) for _ in range(4))
+    dq, dk, dv = oracle.temporal_bwd(q, k, v, do)
+    np.testing.assert_array_equal(dv, do)
+    assert np.all(dq == 0) and np.all(dk == 0)
