@@ -142,6 +142,28 @@ typedef struct {
  * for T = K*N tokens), kept until tsf_destroy. */
 tsf_status tsf_full_block(tsf_handle* h, const tsf_block_weights* w, const tsf_bf16* x, float* y, void* stream);
 
+/* Backward of the attention stages (the paper's TimeSformer
+ * numbers are training runs).  For the forward
+ * o = softmax(s q k^T) v of tsf_temporal_attn / tsf_spatial_attn (s = 1/sqrt d)
+ * and the output gradient dO:
+ *   dv = P^T dO,  dS = P (dO v^T - rowsum(dO o)),  dq = s dS k,  dk = s dS^T q.
+ * P is recomputed (a forward pass that also yields the row statistics), then
+ * one kernel per 128-key tile accumulates dk, dv in TMEM and adds dq into an
+ * fp32 buffer.  All tensors bf16 [K, N, H, d]; fp32 accumulation; outputs must
+ * not overlap inputs or each other.  d in {32, 64} (TSF_ERR_UNSUPPORTED for
+ * d = 128); single-GPU handles.  Workspace allocated on first use. */
+tsf_status tsf_temporal_attn_bwd(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v,
+                                 const tsf_bf16* dO, tsf_bf16* dq, tsf_bf16* dk, tsf_bf16* dv, void* stream);
+tsf_status tsf_spatial_attn_bwd(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v,
+                                const tsf_bf16* dO, tsf_bf16* dq, tsf_bf16* dk, tsf_bf16* dv, void* stream);
+
+/* Backward of tsf_spacetime_block: dx for x (bf16) and dy (fp32), both
+ * [K, N, H, d]:  dX_t = dy + (dq + dk + dv of S at X_t),  dx = dX_t + (dq + dk +
+ * dv of T at x)  (q = k = v in each stage).  X_t is recomputed in bf16 (the
+ * training precision; the forward keeps it in fp16, reading G8), so dx
+ * carries bf16-level error (tests: rel-L2 <= 1e-2).  dx fp32. */
+tsf_status tsf_spacetime_block_bwd(tsf_handle* h, const tsf_bf16* x, const float* dy, float* dx, void* stream);
+
 /* Divided space-time block, temporal then spatial ("followed by"), with
  * identity projections and residual weight 1 (readings G1, G5):
  *   X_t = x + T(x, x, x);   y = X_t + S(X_t, X_t, X_t).
@@ -246,7 +268,8 @@ int tsf_world_size(const tsf_handle* h);
  * stage 0 = temporal attention, 1 = spatial attention, 2 = reshard
  * (all-to-all + unpack), 3 = host<->device copies, 4 = tsf_transpose,
  * 5 = tsf_joint_attn, 6 = tsf_storm_attn, 7 = tsf_full_block GEMMs and
- * LayerNorms (its attention kernels are recorded as stages 0 and 1). */
+ * LayerNorms (its attention kernels are recorded as stages 0 and 1),
+ * 8 = the backward calls. */
 tsf_status tsf_set_timing(tsf_handle* h, int enable);
 tsf_status tsf_stage_ms(tsf_handle* h, int stage, float* total_ms, int* n_records);
 

@@ -42,6 +42,9 @@ SIGNATURES = [
     ("tsf_joint_attn", _I, [_P, _P, _P, _P, _P, _I, _P]),
     ("tsf_storm_attn", _I, [_P, _P, _P, _I, ctypes.c_double, ctypes.c_double, _P, _P]),
     ("tsf_full_block", _I, [_P, _P, _P, _P, _P]),
+    ("tsf_temporal_attn_bwd", _I, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    ("tsf_spatial_attn_bwd", _I, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    ("tsf_spacetime_block_bwd", _I, [_P, _P, _P, _P, _P]),
     ("tsf_spacetime_block", _I, [_P, _P, _P, _P]),
     ("tsf_spacetime_block_host", _I, [_P, _P, _P, _P]),
     ("tsf_destroy", None, [_P]),
@@ -256,6 +259,30 @@ class Layer:
         out = torch.empty(shp, dtype=torch.float32, device=x.device) if out is None else out
         _need(out, torch.float32, shp, "out")
         _check(lib().tsf_full_block(self._h, ctypes.byref(st), x.data_ptr(), out.data_ptr(), _stream_ptr(stream)),
+               self._h)
+        return out
+
+    def attn_bwd(self, axis: int, q, k, v, dO, stream=None):
+        """tsf_temporal_attn_bwd (axis 0) / tsf_spatial_attn_bwd (axis 1): (dq, dk, dv) bf16."""
+        import torch
+        shp = (self.K, self.N, self.H, self.d)
+        for t, n in ((q, "q"), (k, "k"), (v, "v"), (dO, "dO")):
+            _need(t, torch.bfloat16, shp, n)
+        dq, dk, dv = (torch.empty_like(q) for _ in range(3))
+        fn = lib().tsf_temporal_attn_bwd if axis == 0 else lib().tsf_spatial_attn_bwd
+        _check(fn(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), dO.data_ptr(), dq.data_ptr(), dk.data_ptr(),
+                  dv.data_ptr(), _stream_ptr(stream)), self._h)
+        return dq, dk, dv
+
+    def block_bwd(self, x, dy, out=None, stream=None):
+        """tsf_spacetime_block_bwd: x bf16, dy fp32 -> dx fp32 (all [K, N, H, d])."""
+        import torch
+        shp = (self.K, self.N, self.H, self.d)
+        _need(x, torch.bfloat16, shp, "x")
+        _need(dy, torch.float32, shp, "dy")
+        out = torch.empty(shp, dtype=torch.float32, device=x.device) if out is None else out
+        _need(out, torch.float32, shp, "out")
+        _check(lib().tsf_spacetime_block_bwd(self._h, x.data_ptr(), dy.data_ptr(), out.data_ptr(), _stream_ptr(stream)),
                self._h)
         return out
 

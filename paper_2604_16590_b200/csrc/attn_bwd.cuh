@@ -1,0 +1,359 @@
+// Backward pass of one attention stage (the training the
+// paper reports for TimeSformer, PAPER.md P:159-163 / P:509).  For every group
+// (a temporal (n, h) or spatial (t, h) sequence of L tokens):
+//
+//   P = softmax(s Q K^T),  dV = P^T dO,  dP = dO V^T,  dS = P (dP - D),
+//   dQ = s dS K,  dK = s dS^T Q,       D_i = sum_e O_ie dO_ie,  s = 1/sqrt(d)
+//
+// with P recomputed from the forward's row statistic lse2 = log2 sum 2^(s q.k log2e)
+// (flash forward, AttnParams.lse).  One CTA owns a 128-key tile of one group
+// and walks the group's 128-query tiles (FlashAttention-2 order, transposed):
+//
+//   MMA  S^T  = K Q_i^T      (TMEM, keys = lanes)        A = K, B = Q_i   (K-major)
+//   MMA  dP^T = V dO_i^T     (TMEM)                       A = V, B = dO_i  (K-major)
+//   softmax warps (thread = key row): P^T = 2^(S^T s log2e - lse2), dS^T =
+//        P^T (dP^T - D); bf16 P^T over S^T, bf16 dS^T over dP^T (TMEM) and
+//        into a shared-memory tile (the A operand of the dQ MMA)
+//   MMA  dV += P^T dO_i      A = P^T (TMEM), B = dO_i (MN-major)
+//   MMA  dK += dS^T Q_i      A = dS^T (TMEM), B = Q_i (MN-major)
+//   MMA  dQ_i = dS K         A = dS (smem, MN-major), B = K (MN-major) -> TMEM
+//        over S^T; the softmax warps (thread = query row) add s dQ_i into an
+//        fp32 dQ accumulator with vector reductions (red.global.add.v4.f32)
+//   end: dK (times s) and dV rows -> bf16.
+//
+// TMEM (512 columns): S^T / P^T / dQ_i [0,128) | dP^T / dS^T [128,256) |
+// dK [256, 256+d) | dV [256+d, 256+2d).  bf16 operands (the training
+// precision of the paper), fp32 accumulation.  d in {32, 64}.
+//
+// Warps (192 threads): 0-3 softmax / dQ / epilogue, 4 TMA producer, 5 MMA.
+#pragma once
+#include "sm100.cuh"
+#include "attn_common.cuh"
+
+namespace tsf {
+
+struct BwdParams {
+  int L, A, B;                 // sequence length, group dims
+  long long sL, sA, sB;        // element strides of q, k, v, dO, dK, dV, dQacc (same layout)
+  const float* lse;            // [A*B][lse_pitch] group-major, log2 units
+  const float* drow;           // [A*B][lse_pitch]
+  int lse_pitch;               // >= ceil(L / 128) * 128
+  float scale;                 // 1 / sqrt(d)
+  float scale_log2;            // log2(e) / sqrt(d)
+  float* dq;                   // fp32 accumulator (zeroed by the host)
+  __nv_bfloat16* dk;
+  __nv_bfloat16* dv;
+  int nkt, nqt;                // 128-row key / query tiles per group
+};
+
+TSF_DEV void bulk_load_1d(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+TSF_DEV void red_add_v4(float* gaddr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(gaddr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+template <int D>
+struct BwdCfg {
+  static constexpr int SWB = (2 * D < 128) ? 2 * D : 128;
+  static constexpr int CH = SWB / 2;
+  static constexpr int NCH = D / CH;
+  static constexpr int CHUNK = 128 * SWB;                 // one column chunk of a 128-row tile
+  static constexpr int TILE = NCH * CHUNK;                // 128 x D bf16
+  static constexpr int STAGE = 2 * TILE + 2 * 512;        // Q_i, dO_i, lse2_i, D_i
+  static constexpr int NST = 2;
+  static constexpr int DS_BYTES = 128 * 128 * 2;          // dS, MN-major A operand (2 chunks of 64 queries)
+  static constexpr int SMEM = 2 * TILE + NST * STAGE + DS_BYTES + 256 + 1024;
+  static constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DK = 256, COL_DV = 256 + D;
+};
+
+template <int D>
+__global__ void __launch_bounds__(192, 1)
+attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
+                const BwdParams p) {
+  using C = BwdCfg<D>;
+  constexpr int NST = C::NST;
+  constexpr uint32_t swz = (C::SWB == 128) ? SWZ_128B : SWZ_64B;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = smem + C::TILE;
+  uint8_t* sSt = smem + 2 * C::TILE;                      // NST stages
+  uint8_t* sDS = sSt + NST * C::STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + C::DS_BYTES);
+  uint64_t* kv_full = bars;
+  uint64_t* st_full = bars + 1;          // [NST]
+  uint64_t* st_empty = bars + 1 + NST;   // [NST]
+  uint64_t* s_full = bars + 1 + 2 * NST;
+  uint64_t* p_full = s_full + 1;         // 4 softmax warps
+  uint64_t* dq_full = s_full + 2;
+  uint64_t* dq_empty = s_full + 3;       // 4 warps
+  uint64_t* dkv_full = s_full + 4;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_full + 5);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int kt = blockIdx.x % p.nkt;
+  const int grp = blockIdx.x / p.nkt;
+  const int ga = grp % p.A, gb = grp / p.A;
+  const int nq = p.nqt;
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&st_full[s], 1);
+      mbar_init(&st_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 4);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, 4);
+    mbar_init(dkv_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<512>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 4) {
+    // ===================== TMA producer =====================
+    if (elect_one()) {
+      mbar_arrive_expect_tx(kv_full, 2 * C::TILE);
+#pragma unroll
+      for (int c = 0; c < C::NCH; ++c) {
+        tma_load_4d(sK + c * C::CHUNK, &tk, kv_full, c * C::CH, kt * 128, ga, gb);
+        tma_load_4d(sV + c * C::CHUNK, &tv, kv_full, c * C::CH, kt * 128, ga, gb);
+      }
+      const long long lbase = (long long)grp * p.lse_pitch;
+      for (int i = 0; i < nq; ++i) {
+        const int s = i % NST;
+        if (i >= NST) mbar_wait_sleep(&st_empty[s], ((i / NST) - 1) & 1);
+        uint8_t* st = sSt + s * C::STAGE;
+        mbar_arrive_expect_tx(&st_full[s], C::STAGE);
+#pragma unroll
+        for (int c = 0; c < C::NCH; ++c) {
+          tma_load_4d(st + c * C::CHUNK, &tq, &st_full[s], c * C::CH, i * 128, ga, gb);
+          tma_load_4d(st + C::TILE + c * C::CHUNK, &tdo, &st_full[s], c * C::CH, i * 128, ga, gb);
+        }
+        bulk_load_1d(st + 2 * C::TILE, p.lse + lbase + i * 128, 512, &st_full[s]);
+        bulk_load_1d(st + 2 * C::TILE + 512, p.drow + lbase + i * 128, 512, &st_full[s]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ===================== MMA issuer =====================
+    if (elect_one()) {
+      constexpr uint32_t id_kk = make_idesc(128, 128, 0, 0, false);   // S^T, dP^T: both K-major
+      constexpr uint32_t id_tn = make_idesc(128, D, 0, 1, false);     // dV, dK: A TMEM, B MN-major
+      constexpr uint32_t id_nn = make_idesc(128, D, 1, 1, false);     // dQ: A, B MN-major
+      const uint32_t ka = smem_u32(sK), va = smem_u32(sV), dsa = smem_u32(sDS);
+      mbar_wait_sleep(kv_full, 0);
+      for (int i = 0; i < nq; ++i) {
+        const int s = i % NST;
+        mbar_wait_sleep(&st_full[s], (i / NST) & 1);
+        if (i > 0) mbar_wait(dq_empty, (i - 1) & 1);      // S^T region: dQ_(i-1) read
+        tc_fence_after();
+        const uint32_t qa = smem_u32(sSt + s * C::STAGE), doa = qa + C::TILE;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k * 16 / C::CH) * C::CHUNK + (k * 16 % C::CH) * 2;
+          mma_ss(tmem + C::COL_S, make_sdesc(ka + off, 16, 8 * C::SWB, swz), make_sdesc(qa + off, 16, 8 * C::SWB, swz),
+                 id_kk, k > 0);
+        }
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k * 16 / C::CH) * C::CHUNK + (k * 16 % C::CH) * 2;
+          mma_ss(tmem + C::COL_DP, make_sdesc(va + off, 16, 8 * C::SWB, swz),
+                 make_sdesc(doa + off, 16, 8 * C::SWB, swz), id_kk, k > 0);
+        }
+        mma_commit(s_full);
+        mbar_wait(p_full, i & 1);
+        tc_fence_after();
+        // dV += P^T dO_i, dK += dS^T Q_i   (K = 128 queries in steps of 16; B MN-major)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          mma_ts(tmem + C::COL_DV, tmem + C::COL_S + 8 * k,
+                 make_sdesc(doa + k * 16 * C::SWB, C::CHUNK, 8 * C::SWB, swz), id_tn, (i > 0 || k > 0) ? 1u : 0u);
+          mma_ts(tmem + C::COL_DK, tmem + C::COL_DP + 8 * k,
+                 make_sdesc(qa + k * 16 * C::SWB, C::CHUNK, 8 * C::SWB, swz), id_tn, (i > 0 || k > 0) ? 1u : 0u);
+        }
+        // dQ_i = dS K   (M = 128 queries, K = 128 keys; A = dS in smem, MN-major,
+        // 2 chunks of 64 queries; B = K tile, MN-major) -> over S^T
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          mma_ss(tmem + C::COL_S, make_sdesc(dsa + k * 16 * 128, 128 * 128, 8 * 128, SWZ_128B),
+                 make_sdesc(ka + k * 16 * C::SWB, C::CHUNK, 8 * C::SWB, swz), id_nn, k > 0);
+        mma_commit(dq_full);
+        mma_commit(&st_empty[s]);
+      }
+      mma_commit(dkv_full);
+    }
+    __syncwarp();
+  } else {
+    // ===================== softmax / dQ / epilogue (warps 0-3) =====================
+    const uint32_t r = warp * 32 + lane;                    // TMEM lane
+    const uint32_t lane_base = (warp * 32) << 16;
+    const bool key_ok = kt * 128 + (int)r < p.L;
+    const float sl2 = p.scale_log2;
+    for (int i = 0; i < nq; ++i) {
+      const int s = i % NST;
+      const uint8_t* st = sSt + s * C::STAGE;
+      const float* lse = reinterpret_cast<const float*>(st + 2 * C::TILE);
+      const float* dr = reinterpret_cast<const float*>(st + 2 * C::TILE + 512);
+      const int qvalid = p.L - i * 128;                     // queries >= qvalid are padding
+      mbar_wait(s_full, i & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t sv[32], dv[32];
+        tmem_ld_x32(tmem + lane_base + C::COL_S + c0, sv);
+        tmem_ld_x32(tmem + lane_base + C::COL_DP + c0, dv);
+        tmem_wait_ld();
+        uint32_t pp[16], dd[16];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          float pr[2], dsr[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int q = c0 + c + e;
+            const bool ok = key_ok && q < qvalid;
+            const float pv = ok ? ex2(fmaf(__uint_as_float(sv[c + e]), sl2, -lse[q])) : 0.f;
+            pr[e] = pv;
+            dsr[e] = ok ? pv * (__uint_as_float(dv[c + e]) - dr[q]) : 0.f;
+          }
+          pp[c / 2] = pack2<false>(pr[0], pr[1]);
+          dd[c / 2] = pack2<false>(dsr[0], dsr[1]);
+        }
+        tmem_st_x16(tmem + lane_base + C::COL_S + c0 / 2, pp);
+        tmem_st_x16(tmem + lane_base + C::COL_DP + c0 / 2, dd);
+        // dS (query-contiguous rows of this key) into the MN-major A tile of the dQ MMA
+        uint8_t* chunk = sDS + (c0 / 64) * (128 * 128);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t unit = (uint32_t)((c0 % 64) / 8 + u);
+          *reinterpret_cast<uint4*>(chunk + r * 128 + ((unit ^ (r & 7u)) << 4)) =
+              make_uint4(dd[4 * u], dd[4 * u + 1], dd[4 * u + 2], dd[4 * u + 3]);
+        }
+      }
+      tmem_wait_st();
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      // dQ_i rows (thread = query row): s dQ into the fp32 accumulator
+      mbar_wait(dq_full, i & 1);
+      tc_fence_after();
+      const int qrow = i * 128 + (int)r;
+#pragma unroll
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t qv[32];
+        tmem_ld_x32(tmem + lane_base + C::COL_S + c0, qv);
+        tmem_wait_ld();
+        if (qrow < p.L) {
+          float* dst = p.dq + (long long)qrow * p.sL + (long long)ga * p.sA + (long long)gb * p.sB + c0;
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            red_add_v4(dst + e, p.scale * __uint_as_float(qv[e]), p.scale * __uint_as_float(qv[e + 1]),
+                       p.scale * __uint_as_float(qv[e + 2]), p.scale * __uint_as_float(qv[e + 3]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_empty);
+    }
+    // ---- dK, dV rows of this key tile ----
+    mbar_wait(dkv_full, 0);
+    tc_fence_after();
+    const int krow = kt * 128 + (int)r;
+    const long long off = (long long)krow * p.sL + (long long)ga * p.sA + (long long)gb * p.sB;
+#pragma unroll
+    for (int c0 = 0; c0 < D; c0 += 32) {
+      uint32_t kv[32], vv[32];
+      tmem_ld_x32(tmem + lane_base + C::COL_DK + c0, kv);
+      tmem_ld_x32(tmem + lane_base + C::COL_DV + c0, vv);
+      tmem_wait_ld();
+      if (key_ok) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 8) {
+          uint4 wk, wv;
+          wk.x = pack2<false>(p.scale * __uint_as_float(kv[e]), p.scale * __uint_as_float(kv[e + 1]));
+          wk.y = pack2<false>(p.scale * __uint_as_float(kv[e + 2]), p.scale * __uint_as_float(kv[e + 3]));
+          wk.z = pack2<false>(p.scale * __uint_as_float(kv[e + 4]), p.scale * __uint_as_float(kv[e + 5]));
+          wk.w = pack2<false>(p.scale * __uint_as_float(kv[e + 6]), p.scale * __uint_as_float(kv[e + 7]));
+          wv.x = pack2<false>(__uint_as_float(vv[e]), __uint_as_float(vv[e + 1]));
+          wv.y = pack2<false>(__uint_as_float(vv[e + 2]), __uint_as_float(vv[e + 3]));
+          wv.z = pack2<false>(__uint_as_float(vv[e + 4]), __uint_as_float(vv[e + 5]));
+          wv.w = pack2<false>(__uint_as_float(vv[e + 6]), __uint_as_float(vv[e + 7]));
+          *reinterpret_cast<uint4*>(p.dk + off + c0 + e) = wk;
+          *reinterpret_cast<uint4*>(p.dv + off + c0 + e) = wv;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// Elementwise helpers of the block backward (HBM-bound, 16-byte vectors).
+// out_f32 = a + b + c + d (fp32 a; bf16 b, c; fp32 d accumulator), and its bf16 copy.
+__global__ void __launch_bounds__(256) sum4_kernel(const float* __restrict__ a, const float* __restrict__ dq,
+                                                   const __nv_bfloat16* __restrict__ dk,
+                                                   const __nv_bfloat16* __restrict__ dv, float* __restrict__ out,
+                                                   __nv_bfloat16* __restrict__ out_bf16, long long n8) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
+    const float4 a0 = reinterpret_cast<const float4*>(a)[2 * i], a1 = reinterpret_cast<const float4*>(a)[2 * i + 1];
+    const float4 q0 = reinterpret_cast<const float4*>(dq)[2 * i], q1 = reinterpret_cast<const float4*>(dq)[2 * i + 1];
+    const uint4 kb = reinterpret_cast<const uint4*>(dk)[i], vb = reinterpret_cast<const uint4*>(dv)[i];
+    const uint32_t ku[4] = {kb.x, kb.y, kb.z, kb.w}, vu[4] = {vb.x, vb.y, vb.z, vb.w};
+    float f[8] = {a0.x + q0.x, a0.y + q0.y, a0.z + q0.z, a0.w + q0.w, a1.x + q1.x, a1.y + q1.y, a1.z + q1.z, a1.w + q1.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 k2 = unpack2<false>(ku[e]), v2 = unpack2<false>(vu[e]);
+      f[2 * e] += k2.x + v2.x;
+      f[2 * e + 1] += k2.y + v2.y;
+    }
+    reinterpret_cast<float4*>(out)[2 * i] = make_float4(f[0], f[1], f[2], f[3]);
+    reinterpret_cast<float4*>(out)[2 * i + 1] = make_float4(f[4], f[5], f[6], f[7]);
+    if (out_bf16)
+      reinterpret_cast<uint4*>(out_bf16)[i] =
+          make_uint4(pack2<false>(f[0], f[1]), pack2<false>(f[2], f[3]), pack2<false>(f[4], f[5]), pack2<false>(f[6], f[7]));
+  }
+}
+
+// out (bf16) = bf16(a_bf16 + b_bf16) and (optionally) fp32 -> bf16 of c
+__global__ void __launch_bounds__(256) add_bf16_kernel(const __nv_bfloat16* __restrict__ a,
+                                                       const __nv_bfloat16* __restrict__ b,
+                                                       __nv_bfloat16* __restrict__ out, long long n8) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
+    const uint4 x = reinterpret_cast<const uint4*>(a)[i], y = reinterpret_cast<const uint4*>(b)[i];
+    const uint32_t xu[4] = {x.x, x.y, x.z, x.w}, yu[4] = {y.x, y.y, y.z, y.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 p = unpack2<false>(xu[e]), q = unpack2<false>(yu[e]);
+      o[e] = pack2<false>(p.x + q.x, p.y + q.y);
+    }
+    reinterpret_cast<uint4*>(out)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+__global__ void __launch_bounds__(256) f32_to_bf16_kernel(const float* __restrict__ a, __nv_bfloat16* __restrict__ out,
+                                                          long long n8) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
+    const float4 a0 = reinterpret_cast<const float4*>(a)[2 * i], a1 = reinterpret_cast<const float4*>(a)[2 * i + 1];
+    reinterpret_cast<uint4*>(out)[i] = make_uint4(pack2<false>(a0.x, a0.y), pack2<false>(a0.z, a0.w),
+                                                  pack2<false>(a1.x, a1.y), pack2<false>(a1.z, a1.w));
+  }
+}
+
+}  // namespace tsf

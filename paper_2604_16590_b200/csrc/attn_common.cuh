@@ -92,6 +92,13 @@ struct AttnParams {
   int Lk;
   // STORM epilogue weight: g for EPI_STORM_X, 1 - g for EPI_STORM_S
   float gate;
+  // backward recompute (EPI_OUT16 flash path only, when lse != null): per query
+  // row, lse2 = log2 sum_j 2^(s_j log2e / sqrt d) (log2 units) and, when dO is
+  // given, D = sum_e O_e dO_e; stored group-major at (gb * A + ga) * lse_pitch + l
+  float* lse;
+  float* drow;
+  const void* dO;
+  int lse_pitch;
 };
 constexpr int FLASH_PINGPONG = 2;
 constexpr int FLASH_RES_GLOBAL = 4;  // flash kernel: block residual from global memory, not the Q tile (diagnostics)

@@ -615,6 +615,26 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[t]);  // the next item's PV may overwrite O_t
       const int l_idx = qp * 256 + t * 128 + (int)row;
+      if constexpr (EPI == EPI_OUT16 && SPLIT == 1) {
+        if (p.lse != nullptr && l_idx < L) {  // backward recompute: row statistics
+          const long long li = ((long long)gb * p.A + ga) * p.lse_pitch + l_idx;
+          p.lse[li] = m_run + log2f(l_run);
+          if (p.dO != nullptr) {
+            const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
+            const uint4* dp = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.dO) + off);
+            float acc = 0.f;
+#pragma unroll
+            for (int u = 0; u < OCOLS / 8; ++u) {
+              const uint4 w = dp[u];
+              const float2 a0 = unpack2<false>(w.x), a1 = unpack2<false>(w.y), a2 = unpack2<false>(w.z),
+                           a3 = unpack2<false>(w.w);
+              acc += o[8 * u] * a0.x + o[8 * u + 1] * a0.y + o[8 * u + 2] * a1.x + o[8 * u + 3] * a1.y +
+                     o[8 * u + 4] * a2.x + o[8 * u + 5] * a2.y + o[8 * u + 6] * a3.x + o[8 * u + 7] * a3.y;
+            }
+            p.drow[li] = acc / l_run;
+          }
+        }
+      }
       bool staged = false;
       if constexpr (C::EPI_STAGE > 0) {
         if (p.P > 1 && RES_SMEM) {

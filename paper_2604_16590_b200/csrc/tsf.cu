@@ -22,6 +22,7 @@
 #include "attn_stream.cuh"
 #include "attn_flash3.cuh"
 #include "gemm.cuh"
+#include "attn_bwd.cuh"
 #include "layout.cuh"
 
 using namespace tsf;
@@ -85,6 +86,14 @@ struct tsf_handle {
   // full-block activation workspace (tsf_full_block), allocated on first use
   void* fb = nullptr;
   size_t fb_bytes = 0;
+  // backward workspace (tsf_*_bwd), allocated on first use
+  void* bw = nullptr;
+  size_t bw_bytes = 0;
+  // backward recompute: row statistics requested from the next flash forward
+  float* st_lse = nullptr;
+  float* st_drow = nullptr;
+  const void* st_dO = nullptr;
+  int st_pitch = 0;
 };
 constexpr int HOST_CHUNKS = 4;
 
@@ -482,6 +491,7 @@ template <int D>
 static tsf_status launch_flash_special(tsf_handle* h, int epi, int mask, cudaStream_t st, const CUtensorMap& mq,
                                        const CUtensorMap& mk, const CUtensorMap& mv, const AttnParams& p) {
   if (mask) return launch_flash_fixed<D, EPI_OUT16, 1>(h, st, mq, mk, mv, p);
+  if (epi == EPI_OUT16) return launch_flash_fixed<D, EPI_OUT16, 0>(h, st, mq, mk, mv, p);
   if (epi == EPI_STORM_X) return launch_flash_fixed<D, EPI_STORM_X, 0>(h, st, mq, mk, mv, p);
   return launch_flash_fixed<D, EPI_STORM_S, 0>(h, st, mq, mk, mv, p);
 }
@@ -521,7 +531,12 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
   p.trace = h->trace;
 #endif
   const bool f16 = (epi == EPI_BLOCK_S);  // X_t lives in fp16; x (BLOCK_T) arrives bf16
-  const bool special = mask != 0 || epi == EPI_STORM_X || epi == EPI_STORM_S;  // flash kernel, fixed settings
+  const bool special = mask != 0 || epi == EPI_STORM_X || epi == EPI_STORM_S ||
+                       h->st_lse != nullptr;  // flash kernel, fixed settings
+  p.lse = h->st_lse;
+  p.drow = h->st_drow;
+  p.dO = h->st_dO;
+  p.lse_pitch = h->st_pitch;
   const bool packed = v.L <= 128 && !special;
   p.mask_mode = mask;
   p.mask_n = h->N;
@@ -664,7 +679,7 @@ static tsf_status alloc_workspace(tsf_handle* h) {
 
 static void free_workspace(tsf_handle* h) {
   for (void* p : {(void*)h->xt, (void*)h->rxt, (void*)h->uxt, (void*)h->xdev, (void*)h->ydev, (void*)h->scratch,
-                  h->fb})
+                  h->fb, h->bw})
     if (p) cudaFree(p);
   if (h->nf_host) cudaFreeHost(const_cast<unsigned int*>(h->nf_host));
   h->xt = h->rxt = h->uxt = nullptr;
@@ -673,6 +688,7 @@ static void free_workspace(tsf_handle* h) {
   h->scratch = nullptr;
   h->nf_host = nullptr;
   h->fb = nullptr;
+  h->bw = nullptr;
 }
 
 // ---------------------------------------------------------------------------
@@ -971,6 +987,187 @@ tsf_status tsf_storm_attn(tsf_handle* h, const tsf_bf16* u, const tsf_bf16* ctx,
   if (s == TSF_OK) s = run_attention(h, vu, u, u, u, EPI_STORM_S, nullptr, y, st, nullptr, nullptr, 0, nullptr, (float)(1.0 - g));
   tm.done();
   return s;
+}
+
+// ---------------------------------------------------------------------------
+// Backward (NEXT-2): forward recompute with row statistics, the key-tile
+// backward kernel (attn_bwd.cuh), small elementwise kernels.
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+static tsf_status bwd_workspace(tsf_handle* h, size_t need) {
+  if (h->bw_bytes >= need) return TSF_OK;
+  if (h->bw) cudaFree(h->bw);
+  h->bw = nullptr;
+  h->bw_bytes = 0;
+  if (cudaMalloc(&h->bw, need) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(h, TSF_ERR_NOMEM, "backward workspace cudaMalloc failed");
+  }
+  h->bw_bytes = need;
+  return TSF_OK;
+}
+
+// Gradients of one attention stage over view v (q, k, v, dO bf16 with the
+// view's strides): dq accumulated in fp32 (dqacc, zeroed here), dk / dv bf16.
+// Workspace: o (bf16, E elements) and the row statistics (lse, drow).
+static tsf_status stage_bwd(tsf_handle* h, const View& v, const void* q, const void* k, const void* vv,
+                            const void* dO, float* dqacc, __nv_bfloat16* dk, __nv_bfloat16* dv, __nv_bfloat16* o_ws,
+                            float* lse, float* drow, cudaStream_t st) {
+  const int d = h->d;
+  const int nt = (v.L + 127) / 128;
+  const int pitch = nt * 128;
+  // 1. forward recompute with lse2 and D = rowsum(O dO)
+  h->st_lse = lse;
+  h->st_drow = drow;
+  h->st_dO = dO;
+  h->st_pitch = pitch;
+  tsf_status s = run_attention(h, v, q, k, vv, EPI_OUT16, o_ws, nullptr, st);
+  h->st_lse = nullptr;
+  h->st_drow = nullptr;
+  h->st_dO = nullptr;
+  h->st_pitch = 0;
+  if (s != TSF_OK) return s;
+  // 2. the key-tile backward
+  const size_t E = (size_t)h->K * h->N * h->H * d;
+  TSF_CUDA(h, cudaMemsetAsync(dqacc, 0, E * sizeof(float), st));
+  CUtensorMap mq, mk, mv, mdo;
+  if ((s = make_map(h, &mq, q, d, v, 128, 1, 1, false)) != TSF_OK) return s;
+  if ((s = make_map(h, &mk, k, d, v, 128, 1, 1, false)) != TSF_OK) return s;
+  if ((s = make_map(h, &mv, vv, d, v, 128, 1, 1, false)) != TSF_OK) return s;
+  if ((s = make_map(h, &mdo, dO, d, v, 128, 1, 1, false)) != TSF_OK) return s;
+  BwdParams bp{};
+  bp.L = v.L; bp.A = v.A; bp.B = v.B;
+  bp.sL = v.sL; bp.sA = v.sA; bp.sB = v.sB;
+  bp.lse = lse; bp.drow = drow; bp.lse_pitch = pitch;
+  bp.scale = (float)(1.0 / std::sqrt((double)d));
+  bp.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
+  bp.dq = dqacc; bp.dk = dk; bp.dv = dv;
+  bp.nkt = nt; bp.nqt = nt;
+  const long long grid = (long long)nt * v.A * v.B;
+  if (grid > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "too many backward tiles");
+  auto go = [&](auto kern, int smem) -> tsf_status {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return fail(h, TSF_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    kern<<<(int)grid, 192, smem, st>>>(mq, mk, mv, mdo, bp);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(h, TSF_ERR_CUDA, std::string("backward launch: ") + cudaGetErrorString(e));
+    h->launches++;
+    return TSF_OK;
+  };
+  if (d == 32) return go(attn_bwd_kernel<32>, BwdCfg<32>::SMEM);
+  return go(attn_bwd_kernel<64>, BwdCfg<64>::SMEM);
+}
+
+static int ew_grid(tsf_handle* h, long long n) {
+  long long g = (n + 255) / 256;
+  const long long cap = (long long)h->num_sms * 8;
+  return (int)(g < 1 ? 1 : g > cap ? cap : g);
+}
+
+// one stage's public backward: bf16 dq / dk / dv
+static tsf_status stage_bwd_public(tsf_handle* h, int axis, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v,
+                                   const tsf_bf16* dO, tsf_bf16* dq, tsf_bf16* dk, tsf_bf16* dv, void* stream) {
+  if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
+  h->launches = 0;
+  if (h->world != 1) return fail(h, TSF_ERR_UNSUPPORTED, "the backward runs on single-GPU handles");
+  if (h->d == 128) return fail(h, TSF_ERR_UNSUPPORTED, "the backward supports d in {32, 64}");
+  const size_t E = (size_t)h->K * h->N * h->H * h->d;
+  for (const void* o : {(const void*)dq, (const void*)dk, (const void*)dv}) {
+    tsf_status s = check_ptrs(h, {q, k, v, dO}, o, E * 2, E * 2);
+    if (s != TSF_OK) return s;
+  }
+  if (overlap(dq, E * 2, dk, E * 2) || overlap(dq, E * 2, dv, E * 2) || overlap(dk, E * 2, dv, E * 2))
+    return fail(h, TSF_ERR_CONFIG, "gradient outputs overlap");
+  const View vw = axis == 0 ? temporal_view(h->K, h->N, h->H, h->d) : spatial_view(h->K, h->N, h->H, h->d);
+  const size_t groups = (size_t)vw.A * vw.B, pitch = (size_t)((vw.L + 127) / 128) * 128;
+  const size_t need = E * 2 + E * 4 + 2 * groups * pitch * 4 + 1024;
+  tsf_status s = bwd_workspace(h, need);
+  if (s != TSF_OK) return s;
+  char* b = static_cast<char*>(h->bw);
+  __nv_bfloat16* o_ws = reinterpret_cast<__nv_bfloat16*>(b);
+  float* dqacc = reinterpret_cast<float*>(b + ((E * 2 + 255) & ~size_t(255)));
+  float* lse = dqacc + E;
+  float* drow = lse + groups * pitch;
+  cudaStream_t st = (cudaStream_t)stream;
+  StageTimer tm(h, st, 8);
+  s = stage_bwd(h, vw, q, k, v, dO, dqacc, reinterpret_cast<__nv_bfloat16*>(dk), reinterpret_cast<__nv_bfloat16*>(dv),
+                o_ws, lse, drow, st);
+  if (s == TSF_OK) {
+    f32_to_bf16_kernel<<<ew_grid(h, (long long)(E / 8)), 256, 0, st>>>(dqacc, reinterpret_cast<__nv_bfloat16*>(dq),
+                                                                       (long long)(E / 8));
+    h->launches++;
+    if (cudaGetLastError() != cudaSuccess) s = fail(h, TSF_ERR_CUDA, "dq conversion launch failed");
+  }
+  tm.done();
+  return s;
+}
+
+extern "C" {
+
+tsf_status tsf_temporal_attn_bwd(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v,
+                                 const tsf_bf16* dO, tsf_bf16* dq, tsf_bf16* dk, tsf_bf16* dv, void* stream) {
+  return stage_bwd_public(h, 0, q, k, v, dO, dq, dk, dv, stream);
+}
+
+tsf_status tsf_spatial_attn_bwd(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v,
+                                const tsf_bf16* dO, tsf_bf16* dq, tsf_bf16* dk, tsf_bf16* dv, void* stream) {
+  return stage_bwd_public(h, 1, q, k, v, dO, dq, dk, dv, stream);
+}
+
+tsf_status tsf_spacetime_block_bwd(tsf_handle* h, const tsf_bf16* x, const float* dy, float* dx, void* stream) {
+  if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
+  h->launches = 0;
+  if (h->world != 1) return fail(h, TSF_ERR_UNSUPPORTED, "the backward runs on single-GPU handles");
+  if (h->d == 128) return fail(h, TSF_ERR_UNSUPPORTED, "the backward supports d in {32, 64}");
+  const size_t E = (size_t)h->K * h->N * h->H * h->d;
+  tsf_status s = check_ptrs(h, {x}, dx, E * 2, E * 4);
+  if (s != TSF_OK) return s;
+  if ((s = check_ptrs(h, {dy}, dx, E * 4, E * 4)) != TSF_OK) return s;
+  const View vt = temporal_view(h->K, h->N, h->H, h->d), vs = spatial_view(h->K, h->N, h->H, h->d);
+  const size_t pt = (size_t)((vt.L + 127) / 128) * 128 * vt.A * vt.B, ps = (size_t)((vs.L + 127) / 128) * 128 * vs.A * vs.B;
+  const size_t pmax = pt > ps ? pt : ps;
+  // o_ws | xtb | dyb | dxtb | dk | dv (bf16, E each) | dqacc | dxt (fp32, E each) | lse | drow
+  const size_t need = 6 * E * 2 + 2 * E * 4 + 2 * pmax * 4 + 4096;
+  if ((s = bwd_workspace(h, need)) != TSF_OK) return s;
+  __nv_bfloat16* o_ws = static_cast<__nv_bfloat16*>(h->bw);
+  __nv_bfloat16* xtb = o_ws + E;
+  __nv_bfloat16* dyb = xtb + E;
+  __nv_bfloat16* dxtb = dyb + E;
+  __nv_bfloat16* dk = dxtb + E;
+  __nv_bfloat16* dv = dk + E;
+  float* dqacc = reinterpret_cast<float*>(dv + E);
+  float* dxt = dqacc + E;
+  float* lse = dxt + E;
+  float* drow = lse + pmax;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long n8 = (long long)(E / 8);
+  const int g = ew_grid(h, n8);
+  int total = 0;
+  auto count = [&]() { total += h->launches; h->launches = 0; };
+  StageTimer tm(h, st, 8);
+  // X_t = x + T(x, x, x) (bf16), dy -> bf16
+  if ((s = run_attention(h, vt, x, x, x, EPI_OUT16, o_ws, nullptr, st)) != TSF_OK) return s;
+  count();
+  add_bf16_kernel<<<g, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(x), o_ws, xtb, n8);
+  f32_to_bf16_kernel<<<g, 256, 0, st>>>(dy, dyb, n8);
+  total += 2;
+  TSF_CUDA(h, cudaGetLastError());
+  // spatial stage: dX_t = dy + dq + dk + dv of S at X_t
+  if ((s = stage_bwd(h, vs, xtb, xtb, xtb, dyb, dqacc, dk, dv, o_ws, lse, drow, st)) != TSF_OK) return s;
+  count();
+  sum4_kernel<<<g, 256, 0, st>>>(dy, dqacc, dk, dv, dxt, dxtb, n8);
+  total++;
+  TSF_CUDA(h, cudaGetLastError());
+  // temporal stage: dx = dX_t + dq + dk + dv of T at x
+  if ((s = stage_bwd(h, vt, x, x, x, dxtb, dqacc, dk, dv, o_ws, lse, drow, st)) != TSF_OK) return s;
+  count();
+  sum4_kernel<<<g, 256, 0, st>>>(dxt, dqacc, dk, dv, dx, nullptr, n8);
+  total++;
+  TSF_CUDA(h, cudaGetLastError());
+  tm.done();
+  h->launches = total;
+  return TSF_OK;
 }
 
 // ---------------------------------------------------------------------------
