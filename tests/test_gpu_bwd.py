@@ -19,10 +19,14 @@ pytestmark = pytest.mark.gpu
 def check(got, want, what):
     got = got.double().cpu().numpy() if torch.is_tensor(got) else got
     err = np.abs(got - want).max()
-    rel = np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30)
-    print(f"{what}: max-abs {err:.3e} ({err / np.abs(want).max():.2%} of max|ref| {np.abs(want).max():.3f}) "
-          f"rel-L2 {rel:.3e}")
-    assert np.all(np.isfinite(got)) and rel <= 2e-2 and err <= 3e-2 * np.abs(want).max(), what
+    ref = np.abs(want).max()
+    if ref == 0.0:   # e.g. K = 1: dq = dk = 0 exactly; the GPU's recomputed P is 1 to rounding
+        print(f"{what}: reference is exactly zero, max |got| {err:.3e}")
+        assert err <= 1e-5, what
+        return
+    rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+    print(f"{what}: max-abs {err:.3e} ({err / ref:.2%} of max|ref| {ref:.3f}) rel-L2 {rel:.3e}")
+    assert np.all(np.isfinite(got)) and rel <= 2e-2 and err <= 3e-2 * ref, what
 
 
 SHAPES = [(4, 64, 2, 32), (8, 300, 2, 64), (200, 4, 2, 64), (3, 130, 1, 64), (1, 257, 2, 64), (130, 3, 2, 32)]
