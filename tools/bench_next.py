@@ -4,6 +4,7 @@
     PAPER.md Table I/II) next to the factorized block at the same shape
   * STORM noise-gated attention (tsf_storm_attn)
   * the full divided block with projections / LN / MLP (tsf_full_block)
+  * the backward of the block and of one spatial stage (tsf_*_bwd)
 
     python tools/bench_next.py [--config C2] [--reps 20]
 
@@ -81,6 +82,18 @@ def main():
                          "gemm_flops": F_gemm, "attention_flops": F_block,
                          "tflops_total": (F_gemm + F_block) / ms / 1e9,
                          "gemm_and_ln_ms_per_step": gemm_ms[0] / (args.reps + 3)}
+    # backward of the block at C2 (NEXT-2): algorithmic flops 2.5x the forward's
+    # attention flops (dV, dP, dQ, dK and S^T recompute: 5 matmuls vs 2), the
+    # forward recompute with row statistics is inside the timed call
+    dy = [torch.randn(K, N, H, d, generator=g, device="cuda") for _ in range(2)]
+    ms = timed(lambda i: layer.block_bwd(xs[i % 2], dy[i % 2]), max(3, args.reps // 2))
+    out["block_backward"] = {"ms": ms, "tokens_per_s": K * N / ms * 1e3, "flops_bwd_2p5x": 2.5 * F_block,
+                             "tflops_bwd_2p5x": 2.5 * F_block / ms / 1e9}
+    q3 = [rnd(K, N, H, d) for _ in range(3)]
+    ms = timed(lambda i: layer.attn_bwd(1, q3[0], q3[1], q3[2], q3[i % 2]), max(3, args.reps // 2))
+    F_sp = 4 * H * d * K * N * N
+    out["spatial_attn_backward"] = {"ms": ms, "tflops_bwd_2p5x": 2.5 * F_sp / ms / 1e9,
+                                    "note": "includes the forward recompute (row statistics) and dq fp32->bf16"}
     for k, v in out.items():
         print(json.dumps({"what": k, **v}), flush=True)
 
