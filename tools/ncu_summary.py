@@ -44,9 +44,9 @@ def to_bytes(val, unit):
     return float(val) * mult
 
 
-def main(tag):
+def main(tag, dst_name=None):
     src = os.path.join(ROOT, "gpurun_out", tag)
-    dst = os.path.join(ROOT, "profiles", tag)
+    dst = os.path.join(ROOT, "profiles", dst_name or tag)
     os.makedirs(dst, exist_ok=True)
     md = [f"# Profile {tag}\n"]
     bench_path = os.path.join(src, "bench.json")
@@ -54,12 +54,13 @@ def main(tag):
         shutil.copy(bench_path, os.path.join(dst, "bench.json"))
         md.append("## bench.py line (plain run, not under ncu)\n\n```\n" + open(bench_path).read().strip() + "\n```\n")
     traffic = {}
-    rep = os.path.join(src, "prof.ncu-rep")
-    if os.path.exists(rep):
+    import glob
+    reps = sorted(glob.glob(os.path.join(src, "*.ncu-rep")))
+    out = []
+    for rep in reps:
         raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(io.StringIO(raw)))
         hdr, units = rows[0], rows[1]
-        out = []
         for r in rows[2:]:
             d = dict(zip(hdr, r))
             u = dict(zip(hdr, units))
@@ -72,7 +73,8 @@ def main(tag):
             rec["dram_bytes_per_launch"] = rb + wb
             out.append(rec)
             tag_k = "spatial_C2" if "flash" in rec["kernel"] else "temporal_C2"
-            traffic.setdefault(tag_k, rb + wb)
+            traffic[tag_k] = rb + wb
+    if out:
         with open(os.path.join(dst, "ncu_full.csv"), "w", newline="") as f:
             w = csv.DictWriter(f, fieldnames=list(out[0].keys()))
             w.writeheader()
@@ -115,4 +117,4 @@ def main(tag):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None)
