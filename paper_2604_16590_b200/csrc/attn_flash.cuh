@@ -543,6 +543,30 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         // SEP: all of P_t is packed in registers and stored after the last
         // exponential, so the wait for PV_t(G-1) (P_t's buffer) is at the end
         uint32_t pk_all[C::SEP ? CW / 2 : 1];
+        if (C::SEP && (p.flags & FLASH_INPLACE_EXP)) {
+          // one dependency graph over all CW columns, transformed in place
+          // (scores -> log2-domain exponents -> P -> packed pairs), so the
+          // scheduler can keep the MUFU queue full across the whole row
+          // instead of draining it at the end of each 32-column pass
+          float f[CW];
+#pragma unroll
+          for (int c = 0; c < CW; c += 2)
+            ffma2(f[c], f[c + 1], __uint_as_float(sv[c]), __uint_as_float(sv[c + 1]), sl2, sl2, nmb, nmb);
+#pragma unroll
+          for (int c = 0; c < CW; c += 2) {
+            if (((c >> 1) & 7) >= 8 - EMU / 2) {
+              ex2_poly2(f[c], f[c + 1], f[c], f[c + 1]);
+            } else {
+              f[c] = ex2(f[c]);
+              f[c + 1] = ex2(f[c + 1]);
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < CW; c += 2) {
+            pk_all[c / 2] = pack2<F16>(f[c], f[c + 1]);
+            if constexpr (!C::ONES) { ls0 += f[c]; ls1 += f[c + 1]; }
+          }
+        } else
 #pragma unroll
         for (int c0 = 0; c0 < CW; c0 += PW) {
           // three passes over PW columns (scale, exponentiate, pack) so no
