@@ -44,6 +44,10 @@ struct BwdParams {
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
   int nkt, nqt;                // 128-row key / query tiles per group
+  // PACKED (L <= 128): one 128-row tile holds G = Ab * Bb whole groups (group-
+  // major rows, as the forward's packed kernel); keys and queries of a group
+  // are in the same tile, so the row statistics are computed in the kernel
+  int Ab, Bb, tiles_a;
 };
 
 TSF_DEV void bulk_load_1d(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -71,7 +75,7 @@ struct BwdCfg {
   static constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DK = 256, COL_DV = 256 + D;
 };
 
-template <int D>
+template <int D, bool PACKED>
 __global__ void __launch_bounds__(192, 1)
 attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                 const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo,
@@ -94,13 +98,39 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   uint64_t* dq_full = s_full + 2;
   uint64_t* dq_empty = s_full + 3;       // 4 warps
   uint64_t* dkv_full = s_full + 4;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_full + 5);
+  uint64_t* st0_full = s_full + 5;       // PACKED: row statistics phase (S, P handed, O)
+  uint64_t* p0_full = s_full + 6;
+  uint64_t* o0_full = s_full + 7;
+  uint64_t* stats_done = s_full + 8;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_full + 9);
 
   const uint32_t warp = warp_id(), lane = lane_id();
-  const int kt = blockIdx.x % p.nkt;
-  const int grp = blockIdx.x / p.nkt;
+  const int kt = PACKED ? 0 : blockIdx.x % p.nkt;
+  const int grp = PACKED ? 0 : blockIdx.x / p.nkt;
   const int ga = grp % p.A, gb = grp / p.A;
-  const int nq = p.nqt;
+  const int nq = PACKED ? 1 : p.nqt;
+  // PACKED: tile coordinates and rows in use; row r is position r % L of group r / L
+  const int a0 = PACKED ? (int)(blockIdx.x % p.tiles_a) * p.Ab : 0;
+  const int b0 = PACKED ? (int)(blockIdx.x / p.tiles_a) * p.Bb : 0;
+  const int Gt = PACKED ? p.Ab * p.Bb : 1;
+  const int rows_used = PACKED ? p.L * Gt : 128;
+  // element offset of tile row r (PACKED: its own group; else the CTA's group)
+  auto row_off = [&](int r, int tile0) -> long long {
+    if constexpr (PACKED) {
+      const int g = r / p.L, l = r - g * p.L;
+      return (long long)l * p.sL + (long long)(a0 + g % p.Ab) * p.sA + (long long)(b0 + g / p.Ab) * p.sB;
+    } else {
+      return (long long)(tile0 + r) * p.sL + (long long)ga * p.sA + (long long)gb * p.sB;
+    }
+  };
+  if constexpr (PACKED) {
+    // rows >= rows_used are never written by TMA: zero all tiles once
+    if (rows_used < 128) {
+      for (uint32_t i = threadIdx.x; i < (2 * C::TILE + NST * C::STAGE) / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+      fence_proxy_async_smem();
+    }
+  }
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
@@ -113,6 +143,10 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 4);
     mbar_init(dkv_full, 1);
+    mbar_init(st0_full, 1);
+    mbar_init(p0_full, 4);
+    mbar_init(o0_full, 1);
+    mbar_init(stats_done, 4);
     fence_barrier_init();
   }
   if (warp == 5) tmem_alloc<512>(tmem_holder);
@@ -124,25 +158,40 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   if (warp == 4) {
     // ===================== TMA producer =====================
     if (elect_one()) {
-      mbar_arrive_expect_tx(kv_full, 2 * C::TILE);
+      const uint32_t tile_bytes = PACKED ? (uint32_t)(C::CH * 2 * rows_used * C::NCH) : (uint32_t)C::TILE;
+      mbar_arrive_expect_tx(kv_full, 2 * tile_bytes);
 #pragma unroll
       for (int c = 0; c < C::NCH; ++c) {
-        tma_load_4d(sK + c * C::CHUNK, &tk, kv_full, c * C::CH, kt * 128, ga, gb);
-        tma_load_4d(sV + c * C::CHUNK, &tv, kv_full, c * C::CH, kt * 128, ga, gb);
+        if constexpr (PACKED) {
+          tma_load_4d(sK + c * C::CHUNK, &tk, kv_full, c * C::CH, 0, a0, b0);
+          tma_load_4d(sV + c * C::CHUNK, &tv, kv_full, c * C::CH, 0, a0, b0);
+        } else {
+          tma_load_4d(sK + c * C::CHUNK, &tk, kv_full, c * C::CH, kt * 128, ga, gb);
+          tma_load_4d(sV + c * C::CHUNK, &tv, kv_full, c * C::CH, kt * 128, ga, gb);
+        }
       }
       const long long lbase = (long long)grp * p.lse_pitch;
       for (int i = 0; i < nq; ++i) {
         const int s = i % NST;
         if (i >= NST) mbar_wait_sleep(&st_empty[s], ((i / NST) - 1) & 1);
         uint8_t* st = sSt + s * C::STAGE;
-        mbar_arrive_expect_tx(&st_full[s], C::STAGE);
+        if constexpr (PACKED) {  // statistics are computed in the kernel
+          mbar_arrive_expect_tx(&st_full[s], 2 * tile_bytes);
 #pragma unroll
-        for (int c = 0; c < C::NCH; ++c) {
-          tma_load_4d(st + c * C::CHUNK, &tq, &st_full[s], c * C::CH, i * 128, ga, gb);
-          tma_load_4d(st + C::TILE + c * C::CHUNK, &tdo, &st_full[s], c * C::CH, i * 128, ga, gb);
+          for (int c = 0; c < C::NCH; ++c) {
+            tma_load_4d(st + c * C::CHUNK, &tq, &st_full[s], c * C::CH, 0, a0, b0);
+            tma_load_4d(st + C::TILE + c * C::CHUNK, &tdo, &st_full[s], c * C::CH, 0, a0, b0);
+          }
+        } else {
+          mbar_arrive_expect_tx(&st_full[s], C::STAGE);
+#pragma unroll
+          for (int c = 0; c < C::NCH; ++c) {
+            tma_load_4d(st + c * C::CHUNK, &tq, &st_full[s], c * C::CH, i * 128, ga, gb);
+            tma_load_4d(st + C::TILE + c * C::CHUNK, &tdo, &st_full[s], c * C::CH, i * 128, ga, gb);
+          }
+          bulk_load_1d(st + 2 * C::TILE, p.lse + lbase + i * 128, 512, &st_full[s]);
+          bulk_load_1d(st + 2 * C::TILE + 512, p.drow + lbase + i * 128, 512, &st_full[s]);
         }
-        bulk_load_1d(st + 2 * C::TILE, p.lse + lbase + i * 128, 512, &st_full[s]);
-        bulk_load_1d(st + 2 * C::TILE + 512, p.drow + lbase + i * 128, 512, &st_full[s]);
       }
     }
     __syncwarp();
@@ -154,6 +203,29 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       constexpr uint32_t id_nn = make_idesc(128, D, 1, 1, false);     // dQ: A, B MN-major
       const uint32_t ka = smem_u32(sK), va = smem_u32(sV), dsa = smem_u32(sDS);
       mbar_wait_sleep(kv_full, 0);
+      if constexpr (PACKED) {
+        // statistics phase: S = Q K^T (queries = lanes), then O = P V
+        constexpr uint32_t id_pv = make_idesc(128, D, 0, 1, false);
+        mbar_wait_sleep(&st_full[0], 0);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(sSt);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k * 16 / C::CH) * C::CHUNK + (k * 16 % C::CH) * 2;
+          mma_ss(tmem + C::COL_S, make_sdesc(qa + off, 16, 8 * C::SWB, swz), make_sdesc(ka + off, 16, 8 * C::SWB, swz),
+                 id_kk, k > 0);
+        }
+        mma_commit(st0_full);
+        mbar_wait(p0_full, 0);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          mma_ts(tmem + C::COL_DP, tmem + C::COL_S + 8 * k,
+                 make_sdesc(va + k * 16 * C::SWB, C::CHUNK, 8 * C::SWB, swz), id_pv, k > 0);
+        mma_commit(o0_full);
+        mbar_wait(stats_done, 0);
+        tc_fence_after();
+      }
       for (int i = 0; i < nq; ++i) {
         const int s = i % NST;
         mbar_wait_sleep(&st_full[s], (i / NST) & 1);
@@ -199,14 +271,82 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
     // ===================== softmax / dQ / epilogue (warps 0-3) =====================
     const uint32_t r = warp * 32 + lane;                    // TMEM lane
     const uint32_t lane_base = (warp * 32) << 16;
-    const bool key_ok = kt * 128 + (int)r < p.L;
+    const bool key_ok = PACKED ? (int)r < rows_used : kt * 128 + (int)r < p.L;
     const float sl2 = p.scale_log2;
+    // PACKED: this row's group occupies columns [glo, glo + L) of the tile
+    const int glo = PACKED ? ((int)r / p.L) * p.L : 0;
+    if constexpr (PACKED) {
+      // ---- row statistics (thread = query row r): lse2 = m + log2 l, D = O . dO ----
+      float* lse_s = reinterpret_cast<float*>(sSt + 2 * C::TILE);
+      float* dr_s = reinterpret_cast<float*>(sSt + 2 * C::TILE + 512);
+      mbar_wait(st0_full, 0);
+      tc_fence_after();
+      float m = -INFINITY;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t sv[32];
+        tmem_ld_x32(tmem + lane_base + C::COL_S + c0, sv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const bool ok = key_ok && c0 + c >= glo && c0 + c < glo + p.L;
+          m = ok ? fmaxf(m, __uint_as_float(sv[c])) : m;
+        }
+      }
+      const float mb = (m == -INFINITY) ? 0.f : m * sl2;
+      float l = 0.f;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t sv[32], pp[16];
+        tmem_ld_x32(tmem + lane_base + C::COL_S + c0, sv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          float pr[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool ok = key_ok && c0 + c + e >= glo && c0 + c + e < glo + p.L;
+            pr[e] = ok ? ex2(fmaf(__uint_as_float(sv[c + e]), sl2, -mb)) : 0.f;
+            l += pr[e];
+          }
+          pp[c / 2] = pack2<false>(pr[0], pr[1]);
+        }
+        tmem_st_x16(tmem + lane_base + C::COL_S + c0 / 2, pp);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p0_full);
+      lse_s[r] = mb + log2f(l > 0.f ? l : 1.f);
+      mbar_wait(o0_full, 0);
+      tc_fence_after();
+      float dacc = 0.f;
+#pragma unroll
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t ov[32];
+        tmem_ld_x32(tmem + lane_base + C::COL_DP + c0, ov);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint4 w = tile_row_u4<D, 128>(sSt + C::TILE, r, c0 / 8 + u);   // dO row r
+          const float2 a0 = unpack2<false>(w.x), a1 = unpack2<false>(w.y), a2 = unpack2<false>(w.z),
+                       a3 = unpack2<false>(w.w);
+          const float* o8 = reinterpret_cast<const float*>(ov) + 8 * u;
+          dacc += o8[0] * a0.x + o8[1] * a0.y + o8[2] * a1.x + o8[3] * a1.y + o8[4] * a2.x + o8[5] * a2.y +
+                  o8[6] * a3.x + o8[7] * a3.y;
+        }
+      }
+      dr_s[r] = key_ok && l > 0.f ? dacc / l : 0.f;
+      tc_fence_before();
+      named_bar_sync(1, 128);                                // lse / D of every row visible
+      if (lane == 0) mbar_arrive(stats_done);
+    }
     for (int i = 0; i < nq; ++i) {
       const int s = i % NST;
       const uint8_t* st = sSt + s * C::STAGE;
       const float* lse = reinterpret_cast<const float*>(st + 2 * C::TILE);
       const float* dr = reinterpret_cast<const float*>(st + 2 * C::TILE + 512);
-      const int qvalid = p.L - i * 128;                     // queries >= qvalid are padding
+      const int qvalid = PACKED ? rows_used : p.L - i * 128;  // queries >= qvalid are padding
       mbar_wait(s_full, i & 1);
       tc_fence_after();
 #pragma unroll 1
@@ -222,7 +362,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int q = c0 + c + e;
-            const bool ok = key_ok && q < qvalid;
+            const bool ok = key_ok && q < qvalid && (!PACKED || (q >= glo && q < glo + p.L));
             const float pv = ok ? ex2(fmaf(__uint_as_float(sv[c + e]), sl2, -lse[q])) : 0.f;
             pr[e] = pv;
             dsr[e] = ok ? pv * (__uint_as_float(dv[c + e]) - dr[q]) : 0.f;
@@ -249,14 +389,15 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       // dQ_i rows (thread = query row): s dQ into the fp32 accumulator
       mbar_wait(dq_full, i & 1);
       tc_fence_after();
-      const int qrow = i * 128 + (int)r;
+      const bool q_in = PACKED ? (int)r < rows_used : i * 128 + (int)r < p.L;
+      const long long qoff = row_off((int)r, i * 128);
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 32) {
         uint32_t qv[32];
         tmem_ld_x32(tmem + lane_base + C::COL_S + c0, qv);
         tmem_wait_ld();
-        if (qrow < p.L) {
-          float* dst = p.dq + (long long)qrow * p.sL + (long long)ga * p.sA + (long long)gb * p.sB + c0;
+        if (q_in) {
+          float* dst = p.dq + qoff + c0;
 #pragma unroll
           for (int e = 0; e < 32; e += 4)
             red_add_v4(dst + e, p.scale * __uint_as_float(qv[e]), p.scale * __uint_as_float(qv[e + 1]),
@@ -270,8 +411,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
     // ---- dK, dV rows of this key tile ----
     mbar_wait(dkv_full, 0);
     tc_fence_after();
-    const int krow = kt * 128 + (int)r;
-    const long long off = (long long)krow * p.sL + (long long)ga * p.sA + (long long)gb * p.sB;
+    const long long off = row_off((int)r, kt * 128);
 #pragma unroll
     for (int c0 = 0; c0 < D; c0 += 32) {
       uint32_t kv[32], vv[32];

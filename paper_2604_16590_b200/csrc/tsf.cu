@@ -1017,6 +1017,45 @@ static tsf_status stage_bwd(tsf_handle* h, const View& v, const void* q, const v
   const int d = h->d;
   const int nt = (v.L + 127) / 128;
   const int pitch = nt * 128;
+  const size_t E0 = (size_t)h->K * h->N * h->H * d;
+  if (v.L <= 128) {
+    // packed: G = 128 / L whole groups per tile, row statistics computed in the
+    // kernel (no forward recompute), one launch
+    const int G = 128 / v.L;
+    int Ab = 1;
+    for (int a = 1; a <= G && a <= v.A; ++a)
+      if (v.A % a == 0) Ab = a;
+    int Bb = G / Ab;
+    if (Bb > v.B) Bb = v.B;
+    CUtensorMap mq, mk, mv, mdo;
+    tsf_status s;
+    if ((s = make_map(h, &mq, q, d, v, v.L, Ab, Bb, false)) != TSF_OK) return s;
+    if ((s = make_map(h, &mk, k, d, v, v.L, Ab, Bb, false)) != TSF_OK) return s;
+    if ((s = make_map(h, &mv, vv, d, v, v.L, Ab, Bb, false)) != TSF_OK) return s;
+    if ((s = make_map(h, &mdo, dO, d, v, v.L, Ab, Bb, false)) != TSF_OK) return s;
+    TSF_CUDA(h, cudaMemsetAsync(dqacc, 0, E0 * sizeof(float), st));
+    BwdParams bp{};
+    bp.L = v.L; bp.A = v.A; bp.B = v.B;
+    bp.sL = v.sL; bp.sA = v.sA; bp.sB = v.sB;
+    bp.scale = (float)(1.0 / std::sqrt((double)d));
+    bp.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
+    bp.dq = dqacc; bp.dk = dk; bp.dv = dv;
+    bp.nkt = 1; bp.nqt = 1;
+    bp.Ab = Ab; bp.Bb = Bb; bp.tiles_a = v.A / Ab;
+    const long long grid = (long long)bp.tiles_a * ((v.B + Bb - 1) / Bb);
+    if (grid > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "too many backward tiles");
+    auto go = [&](auto kern, int smem) -> tsf_status {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return fail(h, TSF_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+      kern<<<(int)grid, 192, smem, st>>>(mq, mk, mv, mdo, bp);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return fail(h, TSF_ERR_CUDA, std::string("backward launch: ") + cudaGetErrorString(e));
+      h->launches++;
+      return TSF_OK;
+    };
+    if (d == 32) return go(attn_bwd_kernel<32, true>, BwdCfg<32>::SMEM);
+    return go(attn_bwd_kernel<64, true>, BwdCfg<64>::SMEM);
+  }
   // 1. forward recompute with lse2 and D = rowsum(O dO)
   h->st_lse = lse;
   h->st_drow = drow;
@@ -1055,8 +1094,8 @@ static tsf_status stage_bwd(tsf_handle* h, const View& v, const void* q, const v
     h->launches++;
     return TSF_OK;
   };
-  if (d == 32) return go(attn_bwd_kernel<32>, BwdCfg<32>::SMEM);
-  return go(attn_bwd_kernel<64>, BwdCfg<64>::SMEM);
+  if (d == 32) return go(attn_bwd_kernel<32, false>, BwdCfg<32>::SMEM);
+  return go(attn_bwd_kernel<64, false>, BwdCfg<64>::SMEM);
 }
 
 static int ew_grid(tsf_handle* h, long long n) {

@@ -47,7 +47,8 @@ def test_stage_bwd_matches_oracle(tsf_lib, shape, axis):
         check(g, w, f"{'temporal' if axis == 0 else 'spatial'} bwd {shape} {n}")
 
 
-@pytest.mark.parametrize("shape", [(4, 64, 2, 32), (8, 300, 2, 64), (6, 260, 2, 64), (200, 4, 2, 64)])
+@pytest.mark.parametrize("shape", [(4, 64, 2, 32), (8, 300, 2, 64), (6, 260, 2, 64), (200, 4, 2, 64),
+                                   (8, 1024, 8, 64)])   # C2-like: K = 8 temporal (packed), N = 1024 spatial
 def test_block_bwd_matches_oracle(tsf_lib, shape):
     K, N, H, d = shape
     xb = synth.make_x(K, N, H, d, seed=63)
