@@ -7,6 +7,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <chrono>
 #include <cmath>
@@ -193,24 +194,37 @@ static cudaEvent_t pool_event(tsf_handle* h) {
   cudaEventCreate(&e);
   return e;
 }
+// NVTX range per stage (host-side enqueue span; a no-op unless a tool such as
+// nsys or ncu is attached) plus, with tsf_set_timing, CUDA events on the stream.
+static const char* const kStageName[] = {"tsf.temporal", "tsf.spatial", "tsf.exchange", "tsf.copy",
+                                         "tsf.transpose", "tsf.joint", "tsf.storm", "tsf.gemm_ln", "tsf.backward"};
 struct StageTimer {
   tsf_handle* h;
   cudaStream_t s;
   int stage;
   cudaEvent_t e0 = nullptr;
+  bool open = true;
   StageTimer(tsf_handle* h_, cudaStream_t s_, int st) : h(h_), s(s_), stage(st) {
+    nvtxRangePushA(kStageName[st]);
     if (h->timing) {
       e0 = pool_event(h);
       cudaEventRecord(e0, s);
     }
   }
   void done() {
+    if (open) {
+      nvtxRangePop();
+      open = false;
+    }
     if (e0) {
       cudaEvent_t e1 = pool_event(h);
       cudaEventRecord(e1, s);
       h->recs.push_back({stage, e0, e1});
       e0 = nullptr;
     }
+  }
+  ~StageTimer() {
+    if (open) nvtxRangePop();
   }
 };
 
