@@ -271,7 +271,10 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
     // ===================== softmax / dQ / epilogue (warps 0-3) =====================
     const uint32_t r = warp * 32 + lane;                    // TMEM lane
     const uint32_t lane_base = (warp * 32) << 16;
-    const bool key_ok = PACKED ? (int)r < rows_used : kt * 128 + (int)r < p.L;
+    // PACKED: a row is real if it is inside the box and its group's b < B (the
+    // last tile along B may be partial: TMA zero-fills it, nothing is stored)
+    const bool key_ok = PACKED ? ((int)r < rows_used && b0 + ((int)r / p.L) / p.Ab < p.B)
+                               : kt * 128 + (int)r < p.L;
     const float sl2 = p.scale_log2;
     // PACKED: this row's group occupies columns [glo, glo + L) of the tile
     const int glo = PACKED ? ((int)r / p.L) * p.L : 0;
@@ -389,7 +392,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       // dQ_i rows (thread = query row): s dQ into the fp32 accumulator
       mbar_wait(dq_full, i & 1);
       tc_fence_after();
-      const bool q_in = PACKED ? (int)r < rows_used : i * 128 + (int)r < p.L;
+      const bool q_in = PACKED ? key_ok : i * 128 + (int)r < p.L;
       const long long qoff = row_off((int)r, i * 128);
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 32) {
