@@ -16,13 +16,13 @@
 //        into a shared-memory tile (the A operand of the dQ MMA)
 //   MMA  dV += P^T dO_i      A = P^T (TMEM), B = dO_i (MN-major)
 //   MMA  dK += dS^T Q_i      A = dS^T (TMEM), B = Q_i (MN-major)
-//   MMA  dQ_i = dS K         A = dS (smem, MN-major), B = K (MN-major) -> TMEM
-//        over S^T; the softmax warps (thread = query row) add s dQ_i into an
+//   MMA  dQ_i = dS K         A = dS (smem, MN-major), B = K (MN-major) -> TMEM;
+//        the softmax warps (thread = query row) add s dQ_i into an
 //        fp32 dQ accumulator with vector reductions (red.global.add.v4.f32)
 //   end: dK (times s) and dV rows -> bf16.
 //
-// TMEM (512 columns): S^T / P^T / dQ_i [0,128) | dP^T / dS^T [128,256) |
-// dK [256, 256+d) | dV [256+d, 256+2d).  bf16 operands (the training
+// TMEM (512 columns): S^T / P^T [0,128) | dP^T / dS^T [128,256) |
+// dK [256, 256+d) | dV [256+d, 256+2d) | dQ_i [256+2d, 256+3d).  bf16 operands (the training
 // precision of the paper), fp32 accumulation.  d in {32, 64}.
 //
 // Warps (192 threads): 0-3 softmax / dQ / epilogue, 4 TMA producer, 5 MMA.
@@ -72,7 +72,8 @@ struct BwdCfg {
   static constexpr int NST = 2;
   static constexpr int DS_BYTES = 128 * 128 * 2;          // dS, MN-major A operand (2 chunks of 64 queries)
   static constexpr int SMEM = 2 * TILE + NST * STAGE + DS_BYTES + 256 + 1024;
-  static constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DK = 256, COL_DV = 256 + D;
+  static constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DK = 256, COL_DV = 256 + D, COL_DQ = 256 + 2 * D;
+  static_assert(256 + 3 * D <= 512, "TMEM: S^T | dP^T | dK | dV | dQ");
 };
 
 template <int D, bool PACKED>
@@ -229,7 +230,6 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       for (int i = 0; i < nq; ++i) {
         const int s = i % NST;
         mbar_wait_sleep(&st_full[s], (i / NST) & 1);
-        if (i > 0) mbar_wait(dq_empty, (i - 1) & 1);      // S^T region: dQ_(i-1) read
         tc_fence_after();
         const uint32_t qa = smem_u32(sSt + s * C::STAGE), doa = qa + C::TILE;
 #pragma unroll
@@ -256,10 +256,15 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
                  make_sdesc(qa + k * 16 * C::SWB, C::CHUNK, 8 * C::SWB, swz), id_tn, (i > 0 || k > 0) ? 1u : 0u);
         }
         // dQ_i = dS K   (M = 128 queries, K = 128 keys; A = dS in smem, MN-major,
-        // 2 chunks of 64 queries; B = K tile, MN-major) -> over S^T
+        // 2 chunks of 64 queries; B = K tile, MN-major) -> its own columns, so the
+        // next tile's S^T / dP^T MMAs need not wait for the dQ_i readout
+        if (i > 0) {
+          mbar_wait(dq_empty, (i - 1) & 1);
+          tc_fence_after();
+        }
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          mma_ss(tmem + C::COL_S, make_sdesc(dsa + k * 16 * 128, 128 * 128, 8 * 128, SWZ_128B),
+          mma_ss(tmem + C::COL_DQ, make_sdesc(dsa + k * 16 * 128, 128 * 128, 8 * 128, SWZ_128B),
                  make_sdesc(ka + k * 16 * C::SWB, C::CHUNK, 8 * C::SWB, swz), id_nn, k > 0);
         mma_commit(dq_full);
         mma_commit(&st_empty[s]);
@@ -397,7 +402,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += 32) {
         uint32_t qv[32];
-        tmem_ld_x32(tmem + lane_base + C::COL_S + c0, qv);
+        tmem_ld_x32(tmem + lane_base + C::COL_DQ + c0, qv);
         tmem_wait_ld();
         if (q_in) {
           float* dst = p.dq + qoff + c0;
