@@ -39,45 +39,48 @@
 
 namespace tsf {
 
-template <int D, int WIN, int NST>
+template <int D, int WIN, int NST, int NS = 2>
 struct StreamCfg {
   static constexpr int SWB = (2 * D < 128) ? 2 * D : 128;
   static constexpr int CH = SWB / 2;
   static constexpr int NCH = D / CH;
   static constexpr int CHUNK_BYTES = 128 * SWB;
   static constexpr int TILE_BYTES = NCH * CHUNK_BYTES;        // 128 x D 16-bit
-  static constexpr int SLOT = 256;                            // TMEM columns per slot
-  static constexpr int COL_S = 0, COL_P = 128, COL_O = 192;
-  static_assert(192 + D <= SLOT, "two TMEM slots need D <= 64");
+  // NS = 2: slot = [S 128 | P 64 | O 64];  NS = 4: slot = 128 columns, S
+  // [0,128) -> P over [0,64) after the softmax read S -> O over [64,128)
+  static constexpr int SLOT = 512 / NS;                       // TMEM columns per slot
+  static constexpr int COL_S = 0, COL_P = (NS == 4) ? 0 : 128, COL_O = (NS == 4) ? 64 : 192;
+  static_assert(NS == 2 || NS == 4, "TMEM slots");
+  static_assert(COL_O + D <= SLOT, "TMEM slot layout needs D <= 64");
   static_assert(WIN == 32 || WIN == 64, "softmax window");
-  static constexpr int LBUF_BYTES = 2 * 128 * 4;              // l per row per slot
+  static constexpr int LBUF_BYTES = NS * 128 * 4;             // l per row per slot
   static constexpr int BAR_BYTES = 512;
   static constexpr int SMEM = NST * TILE_BYTES + 2 * TILE_BYTES + LBUF_BYTES + BAR_BYTES + 1024;
   static constexpr int THREADS = 640;
   static constexpr int W_EPI = 4, W_CONV = 12, NCONV = 4, W_TMA = 16, W_QK = 17, W_PV = 18;
 };
 
-template <int D, int WIN, int NST, int LT>
+template <int D, int WIN, int NST, int LT, int NS>
 __global__ void __launch_bounds__(640, 1)
 attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap to,
                    const __grid_constant__ PeerMaps pm, const AttnParams p) {
-  using C = StreamCfg<D, WIN, NST>;
+  using C = StreamCfg<D, WIN, NST, NS>;
   static_assert(LT == 0 || (WIN == 32 && 32 % LT == 0 && LT >= 2), "compact softmax: L divides 32");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sIn = smem;                                   // NST input tiles (x, bf16 -> fp16 in place)
   uint8_t* sOut = smem + NST * C::TILE_BYTES;            // fp16 X_t staging tile of each epilogue warpgroup
-  float* lbuf = reinterpret_cast<float*>(sOut + 2 * C::TILE_BYTES);   // [2][128]
+  float* lbuf = reinterpret_cast<float*>(sOut + 2 * C::TILE_BYTES);   // [NS][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + 2 * C::TILE_BYTES + C::LBUF_BYTES);
   uint64_t* in_full = bars;              // [NST] TMA
   uint64_t* in_conv = bars + NST;        // [NST] converter
   uint64_t* in_empty = bars + 2 * NST;   // [NST] epilogue read the residual (4 warps)
-  uint64_t* s_full = bars + 3 * NST;     // [2] QK^T committed
-  uint64_t* p_full = s_full + 2;         // [2] softmax stored P and l (4 warps)
-  uint64_t* o_full = s_full + 4;         // [2] PV committed
-  uint64_t* o_empty = s_full + 6;        // [2] epilogue read O and l (4 warps)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_full + 8);
-  static_assert(sizeof(uint64_t) * (3 * NST + 8) + 4 <= C::BAR_BYTES, "barrier space");
+  uint64_t* s_full = bars + 3 * NST;     // [NS] QK^T committed
+  uint64_t* p_full = s_full + NS;        // [NS] softmax stored P and l (4 warps)
+  uint64_t* o_full = s_full + 2 * NS;    // [NS] PV committed
+  uint64_t* o_empty = s_full + 3 * NS;   // [NS] epilogue read O and l (4 warps)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_full + 4 * NS);
+  static_assert(sizeof(uint64_t) * (3 * NST + 4 * NS) + 4 <= C::BAR_BYTES, "barrier space");
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int L = p.L;
@@ -99,7 +102,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
       mbar_init(&in_conv[s], 1);
       mbar_init(&in_empty[s], 4);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NS; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&p_full[b], 4);
       mbar_init(&o_full[b], 1);
@@ -177,10 +180,13 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
       constexpr uint32_t idesc = make_idesc(128, 128, 0, 0, true);
       constexpr uint32_t swz = C::SWB == 128 ? SWZ_128B : SWZ_64B;
       for (int i = 0; i < my_tiles; ++i) {
-        const int s = i % NST, b = i & 1;
+        const int s = i % NST, b = i % NS;
         mbar_wait_sleep(&in_conv[s], (i / NST) & 1);
-        // S[b] is free once the softmax of tile i - 2 has loaded it (and stored P)
-        if (i >= 2) mbar_wait_sleep(&p_full[b], ((i - 2) >> 1) & 1);
+        if constexpr (NS == 2) {  // S[b] is free once the softmax of tile i - 2 has loaded it (and stored P)
+          if (i >= 2) mbar_wait_sleep(&p_full[b], ((i - 2) >> 1) & 1);
+        } else {                  // the whole slot is free once the epilogue of tile i - 4 has read O
+          if (i >= NS) mbar_wait_sleep(&o_empty[b], ((i - NS) / NS) & 1);
+        }
         TSF_STAMP(p, 12 + (C::W_QK), i);
         tc_fence_after();
         const uint32_t xa = smem_u32(sIn + s * C::TILE_BYTES);
@@ -200,10 +206,11 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
       constexpr uint32_t idesc = make_idesc(128, D, 0, 1, true);
       constexpr uint32_t swz = C::SWB == 128 ? SWZ_128B : SWZ_64B;
       for (int i = 0; i < my_tiles; ++i) {
-        const int s = i % NST, b = i & 1;
-        mbar_wait_sleep(&p_full[b], (i >> 1) & 1);
-        // O[b] is free once the epilogue of tile i - 2 has read it
-        if (i >= 2) mbar_wait_sleep(&o_empty[b], ((i - 2) >> 1) & 1);
+        const int s = i % NST, b = i % NS;
+        mbar_wait_sleep(&p_full[b], (i / NS) & 1);
+        // O[b] is free once the epilogue of tile i - NS has read it (NS = 4:
+        // implied, the QK^T of this tile waited for it)
+        if (NS == 2 && i >= 2) mbar_wait_sleep(&o_empty[b], ((i - 2) >> 1) & 1);
         TSF_STAMP(p, 12 + (C::W_PV), i);
         tc_fence_after();
         const uint32_t va = smem_u32(sIn + s * C::TILE_BYTES);
@@ -224,7 +231,7 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
     const int g = (int)r / L;
     const int lo = g * L - colstart, hi = lo + L;        // this row's window columns [lo, hi)
     const float sl2 = p.scale_log2;
-    {  // P columns outside the windows stay zero in both slots
+    if constexpr (NS == 2) {  // P columns outside the windows stay zero in both slots
       uint32_t z[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) z[i] = 0;
@@ -236,8 +243,8 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
       tmem_wait_st();
     }
     for (int i = 0; i < my_tiles; ++i) {
-      const int b = i & 1;
-      mbar_wait(&s_full[b], (i >> 1) & 1);
+      const int b = i % NS;
+      mbar_wait(&s_full[b], (i / NS) & 1);
       TSF_STAMP(p, 12 + (warp), 4 * i);
       tc_fence_after();
       uint32_t sv[WIN];
@@ -295,14 +302,28 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
       // P[b] and l[b] are free once the epilogue of tile i - 2 has read O[b] and
       // l[b] (which also means PV(i - 2) has consumed P[b])
       TSF_STAMP(p, 12 + (warp), 4 * i + 1);
-      if (i >= 2) {
+      if (NS == 2 && i >= 2) {
         mbar_wait(&o_empty[b], ((i - 2) >> 1) & 1);
         tc_fence_after();
       }
       TSF_STAMP(p, 12 + (warp), 4 * i + 2);
+      if constexpr (NS == 2) {
 #pragma unroll
-      for (int c = 0; c < WIN / 2; c += 16)
-        tmem_st_x16(tmem + lane_base + b * C::SLOT + C::COL_P + colstart / 2 + c, pk + c);
+        for (int c = 0; c < WIN / 2; c += 16)
+          tmem_st_x16(tmem + lane_base + b * C::SLOT + C::COL_P + colstart / 2 + c, pk + c);
+      } else {
+        // P over the slot's first 64 columns: this row's window, zeros elsewhere
+        // (those columns still hold S values of this lane)
+        uint32_t z[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) z[e] = 0u;
+#pragma unroll
+        for (int c = 0; c < 64; c += 16) {
+          const int w = c - colstart / 2;
+          if (w >= 0 && w < WIN / 2) tmem_st_x16(tmem + lane_base + b * C::SLOT + C::COL_P + c, pk + (w & (WIN / 2 - 1)));
+          else tmem_st_x16(tmem + lane_base + b * C::SLOT + C::COL_P + c, z);
+        }
+      }
       lbuf[b * 128 + r] = l;
       tmem_wait_st();
       tc_fence_before();
@@ -322,24 +343,24 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant
     const bool dist = p.P > 1;
     uint8_t* stg = sOut + e * C::TILE_BYTES;
     const uint32_t bar_id = 1 + e;
-    const uint32_t tcol = tmem + lane_base + e * C::SLOT;
     for (int i = (int)e; i < my_tiles; i += 2) {
       const int tile = blockIdx.x + i * gridDim.x;
-      const int s = i % NST;
-      const uint32_t ph = (i >> 1) & 1;
-      mbar_wait(&o_full[e], ph);
-      mbar_wait(&p_full[e], ph);                         // l[e] written (release by the softmax warps)
+      const int s = i % NST, b = i % NS;
+      const uint32_t tcol = tmem + lane_base + b * C::SLOT;
+      const uint32_t ph = (i / NS) & 1;
+      mbar_wait(&o_full[b], ph);
+      mbar_wait(&p_full[b], ph);                         // l[b] written (release by the softmax warps)
       mbar_wait(&in_conv[s], (i / NST) & 1);             // residual rows converted (release by the converter)
       TSF_STAMP(p, 12 + (warp), 4 * (i >> 1));
       tc_fence_after();
       float o[D];
 #pragma unroll
       for (int c = 0; c < D; c += 32) tmem_ld_x32(tcol + C::COL_O + c, reinterpret_cast<uint32_t*>(o + c));
-      const float l = lbuf[e * 128 + r];
+      const float l = lbuf[b * 128 + r];
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&o_empty[e]);
+      if (lane == 0) mbar_arrive(&o_empty[b]);
       TSF_STAMP(p, 12 + (warp), 4 * (i >> 1) + 1);
       // this warpgroup's staging tile is free once its previous store has read it
       if (et == 0) bulk_wait_read0();

@@ -362,23 +362,39 @@ static bool use_stream(int d, int win) {
   return env != 0 && (d == 32 || d == 64) && (win == 32 || win == 64);
 }
 
+static int stream_slots() {  // TMEM slots of the stream kernel: TSF_STREAM_SLOTS = 2 | 4
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("TSF_STREAM_SLOTS");
+    env = e ? atoi(e) : 4;
+  }
+  return env == 2 ? 2 : 4;
+}
+
+template <int D, int WIN, int NS>
+static tsf_status launch_stream_ns(tsf_handle* h, cudaStream_t st, const CUtensorMap& mx, const CUtensorMap& mo,
+                                   const AttnParams& p) {
+  constexpr int NST = 8;
+  using C = StreamCfg<D, WIN, NST, NS>;
+  int grid = h->num_sms;
+  if (grid > p.num_tiles) grid = p.num_tiles;
+  if constexpr (WIN == 32) {  // compact softmax for the short windows (C1 K = 4, C2 K = 8, C2 at P = 2 K = 16)
+    switch (p.L) {
+      case 4: return launch(h, attn_stream_kernel<D, WIN, NST, 4, NS>, grid, C::THREADS, C::SMEM, st, p, mx, mo, h->pm);
+      case 8: return launch(h, attn_stream_kernel<D, WIN, NST, 8, NS>, grid, C::THREADS, C::SMEM, st, p, mx, mo, h->pm);
+      case 16: return launch(h, attn_stream_kernel<D, WIN, NST, 16, NS>, grid, C::THREADS, C::SMEM, st, p, mx, mo, h->pm);
+      default: break;
+    }
+  }
+  return launch(h, attn_stream_kernel<D, WIN, NST, 0, NS>, grid, C::THREADS, C::SMEM, st, p, mx, mo, h->pm);
+}
+
 template <int D, int WIN>
 static tsf_status launch_stream_t(tsf_handle* h, cudaStream_t st, const CUtensorMap& mx, const CUtensorMap& mo,
                                   const AttnParams& p) {
   if constexpr (D <= 64 && WIN <= 64) {
-    constexpr int NST = 8;
-    using C = StreamCfg<D, WIN, NST>;
-    int grid = h->num_sms;
-    if (grid > p.num_tiles) grid = p.num_tiles;
-    if constexpr (WIN == 32) {  // compact softmax for the short windows (C1 K = 4, C2 K = 8, C2 at P = 2 K = 16)
-      switch (p.L) {
-        case 4: return launch(h, attn_stream_kernel<D, WIN, NST, 4>, grid, C::THREADS, C::SMEM, st, p, mx, mo, h->pm);
-        case 8: return launch(h, attn_stream_kernel<D, WIN, NST, 8>, grid, C::THREADS, C::SMEM, st, p, mx, mo, h->pm);
-        case 16: return launch(h, attn_stream_kernel<D, WIN, NST, 16>, grid, C::THREADS, C::SMEM, st, p, mx, mo, h->pm);
-        default: break;
-      }
-    }
-    return launch(h, attn_stream_kernel<D, WIN, NST, 0>, grid, C::THREADS, C::SMEM, st, p, mx, mo, h->pm);
+    if (stream_slots() == 2) return launch_stream_ns<D, WIN, 2>(h, st, mx, mo, p);
+    return launch_stream_ns<D, WIN, 4>(h, st, mx, mo, p);
   }
   return fail(h, TSF_ERR_UNSUPPORTED, "stream kernel shape");
 }
