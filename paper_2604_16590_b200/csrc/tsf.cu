@@ -362,13 +362,16 @@ static bool use_stream(int d, int win) {
   return env != 0 && (d == 32 || d == 64) && (win == 32 || win == 64);
 }
 
-static int stream_slots() {  // TMEM slots of the stream kernel: TSF_STREAM_SLOTS = 2 | 4
+// TMEM slots of the stream kernel: TSF_STREAM_SLOTS = 2 | 4.  Four slots (S, P, O
+// aliased in 128 columns) measured no faster at C2 (34.7 vs 34.3 us, tools/_r2m.sh,
+// trace 1831 vs 1773 cycles per tile): the stage is not limited by tiles in flight.
+static int stream_slots() {
   static int env = -2;
   if (env == -2) {
     const char* e = getenv("TSF_STREAM_SLOTS");
-    env = e ? atoi(e) : 4;
+    env = e ? atoi(e) : 2;
   }
-  return env == 2 ? 2 : 4;
+  return env == 4 ? 4 : 2;
 }
 
 template <int D, int WIN, int NS>
