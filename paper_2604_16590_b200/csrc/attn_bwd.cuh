@@ -48,6 +48,7 @@ struct BwdParams {
   // major rows, as the forward's packed kernel); keys and queries of a group
   // are in the same tile, so the row statistics are computed in the kernel
   int Ab, Bb, tiles_a;
+  int flags;                   // diagnostics: 1 = skip the dQ reductions (timing only, wrong dq)
 };
 
 TSF_DEV void bulk_load_1d(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -404,7 +405,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         uint32_t qv[32];
         tmem_ld_x32(tmem + lane_base + C::COL_DQ + c0, qv);
         tmem_wait_ld();
-        if (q_in) {
+        if (q_in && !(p.flags & 1)) {
           float* dst = p.dq + qoff + c0;
 #pragma unroll
           for (int e = 0; e < 32; e += 4)

@@ -396,6 +396,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     for (int k = 0; k < my_items; ++k, G0 += nkv) {
       int qp, ga, gb;
       item_coords(k, qp, ga, gb);
+      if (k < 256) TSF_STAMP(p, warp, 512 + 2 * k);      // item start
       float m_run = -INFINITY;  // running max, log2-scaled units
       float l_run = 0.f;        // used when !ONES
 
@@ -621,6 +622,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         TSF_STAMP(p, warp, 7 * i + 6);
       }
 
+      if (k < 256) TSF_STAMP(p, warp, 512 + 2 * k + 1);  // last P handed, epilogue next
       // ---- epilogue of item k: this warp's OCOLS columns of its rows ----
       mbar_wait(&o_done[t], k & 1);
       tc_fence_after();

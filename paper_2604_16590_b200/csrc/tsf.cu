@@ -1116,6 +1116,7 @@ static tsf_status stage_bwd(tsf_handle* h, const View& v, const void* q, const v
   bp.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)d));
   bp.dq = dqacc; bp.dk = dk; bp.dv = dv;
   bp.nkt = nt; bp.nqt = nt;
+  if (const char* e = getenv("TSF_BWD_FLAGS")) bp.flags = atoi(e);
   const long long grid = (long long)nt * v.A * v.B;
   if (grid > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "too many backward tiles");
   auto go = [&](auto kern, int smem) -> tsf_status {

@@ -61,6 +61,14 @@ def main():
     for i in range(min(6, nsub)):
         print(i, (a[0, 7 * i:7 * i + 7] - t0).tolist(), (a[4 * split, 7 * i:7 * i + 7] - t0).tolist(),
               (a[wmma, 4 * i:4 * i + 4] - t0).tolist())
+    # item level (softmax warp 0): item start / last P handed, for up to 256 items
+    it = a[0, 512:1024].reshape(256, 2)
+    n_it = int(np.count_nonzero(it[:, 0]))
+    if n_it > 1:
+        dur = np.diff(it[:n_it, 0])
+        body = it[:n_it, 1] - it[:n_it, 0]
+        print(f"items in CTA0: {n_it}; cycles per item {dur.mean():.0f} = steps {body[:-1].mean():.0f} "
+              f"({body[:-1].mean() / nsub:.0f} per step) + epilogue/transition {(dur - body[:-1]).mean():.0f}")
     os.makedirs("gpurun_out", exist_ok=True)
     np.save("gpurun_out/trace_flash.npy", a)
 
