@@ -392,112 +392,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     constexpr int OCOLS = D / SPLIT;                           // O columns this warp rescales / stores
     const float sl2 = p.scale_log2;
     const bool pingpong = (p.flags & FLASH_PINGPONG) != 0;
-    // ---- epilogue of item k: this warp's OCOLS columns of its rows (a lambda:
-    // with the SEP layout it runs inside step 0 of item k + 1, after that step's
-    // exponentials, so the wait for item k's last PV and the O readout overlap
-    // work instead of stalling the softmax warps between items) ----
-    auto epilogue = [&](const int k, const int qp, const int ga, const int gb, const float m_run, float l_run) {
-      mbar_wait(&o_done[t], k & 1);
-      tc_fence_after();
-      float o[OCOLS];
-#pragma unroll
-      for (int c = 0; c < OCOLS; c += 32) tmem_ld_x32(tOrow + hf * OCOLS + c, reinterpret_cast<uint32_t*>(o + c));
-      if constexpr (C::ONES) {
-        uint32_t lv[8];
-        tmem_ld_x8(tOrow + D, lv);
-        tmem_wait_ld();
-        l_run = __uint_as_float(lv[0]);
-      } else {
-        tmem_wait_ld();
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_empty[t]);  // the next item's PV may overwrite O_t
-      const int l_idx = qp * 256 + t * 128 + (int)row;
-      if constexpr (EPI == EPI_OUT16 && SPLIT == 1) {
-        if (p.lse != nullptr && l_idx < L) {  // backward recompute: row statistics
-          const long long li = ((long long)gb * p.A + ga) * p.lse_pitch + l_idx;
-          p.lse[li] = m_run + log2f(l_run);
-          if (p.dO != nullptr) {
-            const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
-            const uint4* dp = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.dO) + off);
-            float acc = 0.f;
-#pragma unroll
-            for (int u = 0; u < OCOLS / 8; ++u) {
-              const uint4 w = dp[u];
-              const float2 a0 = unpack2<false>(w.x), a1 = unpack2<false>(w.y), a2 = unpack2<false>(w.z),
-                           a3 = unpack2<false>(w.w);
-              acc += o[8 * u] * a0.x + o[8 * u + 1] * a0.y + o[8 * u + 2] * a1.x + o[8 * u + 3] * a1.y +
-                     o[8 * u + 4] * a2.x + o[8 * u + 5] * a2.y + o[8 * u + 6] * a3.x + o[8 * u + 7] * a3.y;
-            }
-            p.drow[li] = acc / l_run;
-          }
-        }
-      }
-      bool staged = false;
-      if constexpr (C::EPI_STAGE > 0) {
-        if (p.P > 1 && RES_SMEM) {
-          // distributed temporal stage: X_t rows staged per warp, then written
-          // to their owner ranks (frame l belongs to rank l / Kc) UPR lanes per row
-          staged = true;
-          uint8_t* stw = sEpi + warp * (32 * 2 * D);
-          const bool ok = l_idx < L;
-          int dst = 0;
-          long long off = 0;
-          if (ok) {
-            dst = l_idx / p.Kc;
-            off = (long long)(l_idx - dst * p.Kc) * p.osL + (long long)ga * p.osA + (long long)(gb + p.b_off) * p.osB;
-            report_nonfinite(p, epilogue_row_stage<D, 128, 32>(o, 1.0f / l_run, sQ + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE, row, stw,
-                                           lane));
-          }
-          __syncwarp();
-          constexpr int UPR = 2 * D / 16;  // 16-byte units per row
-          constexpr int RPI = 32 / UPR;    // rows per warp store
-#pragma unroll
-          for (int j = 0; j < 32 / RPI; ++j) {
-            const int r = j * RPI + (int)lane / UPR, u = (int)lane % UPR;
-            const int rd = __shfl_sync(0xffffffffu, dst, r);
-            const long long ro = __shfl_sync(0xffffffffu, off, r);
-            const int rok = __shfl_sync(0xffffffffu, (int)ok, r);
-            if (rok)
-              *reinterpret_cast<uint4*>(static_cast<__half*>(p.peer_out[rd]) + ro + 8 * u) = tile_row_u4<D, 32>(stw, r, u);
-          }
-          __syncwarp();  // the staging tile is rewritten at the next item
-        }
-      }
-      if (l_idx < L && !staged) {
-        const long long in_off = (long long)l_idx * p.sL + (long long)ga * p.sA + (long long)gb * p.sB;
-        constexpr int NU = OCOLS / 8;
-        if (EPI == EPI_BLOCK_T && p.P > 1) {
-          // distributed temporal stage: frame l_idx belongs to rank l_idx / Kc
-          const int dst = l_idx / p.Kc;
-          AttnParams q = p;
-          q.o = p.peer_out[dst];
-          const long long off = (long long)(l_idx - dst * p.Kc) * p.osL + (long long)ga * p.osA +
-                                (long long)(gb + p.b_off) * p.osB;
-          if (RES_SMEM_OK && RES_SMEM)
-            report_nonfinite(p, epilogue_row<D, 128, EPI, NU>(q, o, 1.0f / l_run, off,
-                                          sQ + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE, row, hf * NU));
-          else
-            report_nonfinite(p, epilogue_row_g<D, EPI, NU>(q, o, 1.0f / l_run, off, in_off, hf * NU));
-        } else if (RES_SMEM_OK && RES_SMEM) {
-          const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
-          report_nonfinite(p, epilogue_row<D, 128, EPI, NU>(p, o, 1.0f / l_run, off,
-                                        sQ + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE, row, hf * NU));
-        } else {
-          const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
-          report_nonfinite(p, epilogue_row_g<D, EPI, NU>(p, o, 1.0f / l_run, off, in_off, hf * NU));
-        }
-      }
-      if (RES_SMEM) {  // this warp's rows of Q_t (item k) read: the next Q may load
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&q_empty[k % C::QST]);
-      }
-    };
     int G0 = 0;  // global KV tile index of the item's first tile
-    // the item whose epilogue is still to run (SEP: deferred into the next item's step 0)
-    int pend_k = -1, pend_qp = 0, pend_ga = 0, pend_gb = 0;
-    float pend_m = 0.f, pend_l = 0.f;
     for (int k = 0; k < my_items; ++k, G0 += nkv) {
       int qp, ga, gb;
       item_coords(k, qp, ga, gb);
@@ -709,10 +604,6 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
           // ping-pong: hand the MUFU to the other tile's warps as soon as the
           // exponentials are done, before waiting for PV_t(G-1) and storing P
           if (pingpong) named_bar_arrive(2 - t, 256 * SPLIT);
-          if (i == 0 && pend_k >= 0) {  // the previous item's epilogue, overlapping this step
-            epilogue(pend_k, pend_qp, pend_ga, pend_gb, pend_m, pend_l);
-            pend_k = -1;
-          }
           before_p_store();
 #pragma unroll
           for (int c0 = 0; c0 < CW; c0 += PW) {
@@ -732,13 +623,104 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       }
 
       if (k < 256) TSF_STAMP(p, warp, 512 + 2 * k + 1);  // last P handed, epilogue next
-      if constexpr (C::SEP) {
-        pend_k = k; pend_qp = qp; pend_ga = ga; pend_gb = gb; pend_m = m_run; pend_l = l_run;
+      // ---- epilogue of item k: this warp's OCOLS columns of its rows ----
+      mbar_wait(&o_done[t], k & 1);
+      tc_fence_after();
+      float o[OCOLS];
+#pragma unroll
+      for (int c = 0; c < OCOLS; c += 32) tmem_ld_x32(tOrow + hf * OCOLS + c, reinterpret_cast<uint32_t*>(o + c));
+      if constexpr (C::ONES) {
+        uint32_t lv[8];
+        tmem_ld_x8(tOrow + D, lv);
+        tmem_wait_ld();
+        l_run = __uint_as_float(lv[0]);
       } else {
-        epilogue(k, qp, ga, gb, m_run, l_run);
+        tmem_wait_ld();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[t]);  // the next item's PV may overwrite O_t
+      const int l_idx = qp * 256 + t * 128 + (int)row;
+      if constexpr (EPI == EPI_OUT16 && SPLIT == 1) {
+        if (p.lse != nullptr && l_idx < L) {  // backward recompute: row statistics
+          const long long li = ((long long)gb * p.A + ga) * p.lse_pitch + l_idx;
+          p.lse[li] = m_run + log2f(l_run);
+          if (p.dO != nullptr) {
+            const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
+            const uint4* dp = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.dO) + off);
+            float acc = 0.f;
+#pragma unroll
+            for (int u = 0; u < OCOLS / 8; ++u) {
+              const uint4 w = dp[u];
+              const float2 a0 = unpack2<false>(w.x), a1 = unpack2<false>(w.y), a2 = unpack2<false>(w.z),
+                           a3 = unpack2<false>(w.w);
+              acc += o[8 * u] * a0.x + o[8 * u + 1] * a0.y + o[8 * u + 2] * a1.x + o[8 * u + 3] * a1.y +
+                     o[8 * u + 4] * a2.x + o[8 * u + 5] * a2.y + o[8 * u + 6] * a3.x + o[8 * u + 7] * a3.y;
+            }
+            p.drow[li] = acc / l_run;
+          }
+        }
+      }
+      bool staged = false;
+      if constexpr (C::EPI_STAGE > 0) {
+        if (p.P > 1 && RES_SMEM) {
+          // distributed temporal stage: X_t rows staged per warp, then written
+          // to their owner ranks (frame l belongs to rank l / Kc) UPR lanes per row
+          staged = true;
+          uint8_t* stw = sEpi + warp * (32 * 2 * D);
+          const bool ok = l_idx < L;
+          int dst = 0;
+          long long off = 0;
+          if (ok) {
+            dst = l_idx / p.Kc;
+            off = (long long)(l_idx - dst * p.Kc) * p.osL + (long long)ga * p.osA + (long long)(gb + p.b_off) * p.osB;
+            report_nonfinite(p, epilogue_row_stage<D, 128, 32>(o, 1.0f / l_run, sQ + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE, row, stw,
+                                           lane));
+          }
+          __syncwarp();
+          constexpr int UPR = 2 * D / 16;  // 16-byte units per row
+          constexpr int RPI = 32 / UPR;    // rows per warp store
+#pragma unroll
+          for (int j = 0; j < 32 / RPI; ++j) {
+            const int r = j * RPI + (int)lane / UPR, u = (int)lane % UPR;
+            const int rd = __shfl_sync(0xffffffffu, dst, r);
+            const long long ro = __shfl_sync(0xffffffffu, off, r);
+            const int rok = __shfl_sync(0xffffffffu, (int)ok, r);
+            if (rok)
+              *reinterpret_cast<uint4*>(static_cast<__half*>(p.peer_out[rd]) + ro + 8 * u) = tile_row_u4<D, 32>(stw, r, u);
+          }
+          __syncwarp();  // the staging tile is rewritten at the next item
+        }
+      }
+      if (l_idx < L && !staged) {
+        const long long in_off = (long long)l_idx * p.sL + (long long)ga * p.sA + (long long)gb * p.sB;
+        constexpr int NU = OCOLS / 8;
+        if (EPI == EPI_BLOCK_T && p.P > 1) {
+          // distributed temporal stage: frame l_idx belongs to rank l_idx / Kc
+          const int dst = l_idx / p.Kc;
+          AttnParams q = p;
+          q.o = p.peer_out[dst];
+          const long long off = (long long)(l_idx - dst * p.Kc) * p.osL + (long long)ga * p.osA +
+                                (long long)(gb + p.b_off) * p.osB;
+          if (RES_SMEM_OK && RES_SMEM)
+            report_nonfinite(p, epilogue_row<D, 128, EPI, NU>(q, o, 1.0f / l_run, off,
+                                          sQ + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE, row, hf * NU));
+          else
+            report_nonfinite(p, epilogue_row_g<D, EPI, NU>(q, o, 1.0f / l_run, off, in_off, hf * NU));
+        } else if (RES_SMEM_OK && RES_SMEM) {
+          const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
+          report_nonfinite(p, epilogue_row<D, 128, EPI, NU>(p, o, 1.0f / l_run, off,
+                                        sQ + (k % C::QST) * C::Q_BYTES + t * C::Q_TILE, row, hf * NU));
+        } else {
+          const long long off = (long long)l_idx * p.osL + (long long)ga * p.osA + (long long)gb * p.osB;
+          report_nonfinite(p, epilogue_row_g<D, EPI, NU>(p, o, 1.0f / l_run, off, in_off, hf * NU));
+        }
+      }
+      if (RES_SMEM) {  // this warp's rows of Q_t (item k) read: the next Q may load
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&q_empty[k % C::QST]);
       }
     }  // items
-    if (pend_k >= 0) epilogue(pend_k, pend_qp, pend_ga, pend_gb, pend_m, pend_l);
     if (pingpong && t == 0 && my_items > 0) named_bar_sync(1, 256 * SPLIT);  // consume tile 1's last turn
   } else {
     // ===================== converter warp (block temporal stage) =====================
