@@ -145,8 +145,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUte
         tmem_wait_ld();
         if (ok) {
           float f[32];
+          const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0 + c0);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]) + __ldg(p.bias + col0 + c0 + j);
+          for (int j = 0; j < 32; j += 4) {
+            const float4 bb = __ldg(b4 + j / 4);
+            f[j] = __uint_as_float(v[j]) + bb.x;
+            f[j + 1] = __uint_as_float(v[j + 1]) + bb.y;
+            f[j + 2] = __uint_as_float(v[j + 2]) + bb.z;
+            f[j + 3] = __uint_as_float(v[j + 3]) + bb.w;
+          }
           const long long off = (long long)row * p.ldc + col0 + c0;
           if constexpr (EPI == GEPI_BIAS_BF16 || EPI == GEPI_GELU_BF16) {
 #pragma unroll
