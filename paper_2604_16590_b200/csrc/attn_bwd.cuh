@@ -22,8 +22,9 @@
 //   end: dK (times s) and dV rows -> bf16.
 //
 // TMEM (512 columns): S^T / P^T [0,128) | dP^T / dS^T [128,256) |
-// dK [256, 256+d) | dV [256+d, 256+2d) | dQ_i [256+2d, 256+3d).  bf16 operands (the training
-// precision of the paper), fp32 accumulation.  d in {32, 64}.
+// dK [256, 256+d) | dV [256+d, 256+2d) | dQ_i [256+2d, 256+3d) (d <= 64; at
+// d = 128 dQ_i goes over S^T).  bf16 operands (the training precision of the
+// paper), fp32 accumulation.  d in {32, 64, 128}.
 //
 // Warps (192 threads): 0-3 softmax / dQ / epilogue, 4 TMA producer, 5 MMA.
 #pragma once
@@ -70,11 +71,16 @@ struct BwdCfg {
   static constexpr int CHUNK = 128 * SWB;                 // one column chunk of a 128-row tile
   static constexpr int TILE = NCH * CHUNK;                // 128 x D bf16
   static constexpr int STAGE = 2 * TILE + 2 * 512;        // Q_i, dO_i, lse2_i, D_i
-  static constexpr int NST = 2;
+  static constexpr int NST = (D == 128) ? 1 : 2;          // d = 128: 64 KB tiles, one stage fits
   static constexpr int DS_BYTES = 128 * 128 * 2;          // dS, MN-major A operand (2 chunks of 64 queries)
   static constexpr int SMEM = 2 * TILE + NST * STAGE + DS_BYTES + 256 + 1024;
-  static constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DK = 256, COL_DV = 256 + D, COL_DQ = 256 + 2 * D;
-  static_assert(256 + 3 * D <= 512, "TMEM: S^T | dP^T | dK | dV | dQ");
+  // dQ_i gets its own columns when they fit (d <= 64); at d = 128 (S^T | dP^T |
+  // dK | dV = 512 columns) it overwrites S^T after the dV MMAs have read P^T
+  static constexpr bool DQ_OWN = (256 + 3 * D <= 512);
+  static constexpr uint32_t COL_S = 0, COL_DP = 128, COL_DK = 256, COL_DV = 256 + D,
+                            COL_DQ = DQ_OWN ? 256 + 2 * D : 0;
+  static_assert(256 + 2 * D <= 512, "TMEM: S^T | dP^T | dK | dV");
+  static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
 template <int D, bool PACKED>
@@ -231,6 +237,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       for (int i = 0; i < nq; ++i) {
         const int s = i % NST;
         mbar_wait_sleep(&st_full[s], (i / NST) & 1);
+        if (!C::DQ_OWN && i > 0) mbar_wait(dq_empty, (i - 1) & 1);   // S^T region: dQ_(i-1) read
         tc_fence_after();
         const uint32_t qa = smem_u32(sSt + s * C::STAGE), doa = qa + C::TILE;
 #pragma unroll
@@ -259,7 +266,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         // dQ_i = dS K   (M = 128 queries, K = 128 keys; A = dS in smem, MN-major,
         // 2 chunks of 64 queries; B = K tile, MN-major) -> its own columns, so the
         // next tile's S^T / dP^T MMAs need not wait for the dQ_i readout
-        if (i > 0) {
+        if (C::DQ_OWN && i > 0) {
           mbar_wait(dq_empty, (i - 1) & 1);
           tc_fence_after();
         }

@@ -1087,6 +1087,7 @@ static tsf_status stage_bwd(tsf_handle* h, const View& v, const void* q, const v
       return TSF_OK;
     };
     if (d == 32) return go(attn_bwd_kernel<32, true>, BwdCfg<32>::SMEM);
+    if (d == 128) return go(attn_bwd_kernel<128, true>, BwdCfg<128>::SMEM);
     return go(attn_bwd_kernel<64, true>, BwdCfg<64>::SMEM);
   }
   // 1. forward recompute with lse2 and D = rowsum(O dO)
@@ -1129,6 +1130,7 @@ static tsf_status stage_bwd(tsf_handle* h, const View& v, const void* q, const v
     return TSF_OK;
   };
   if (d == 32) return go(attn_bwd_kernel<32, false>, BwdCfg<32>::SMEM);
+  if (d == 128) return go(attn_bwd_kernel<128, false>, BwdCfg<128>::SMEM);
   return go(attn_bwd_kernel<64, false>, BwdCfg<64>::SMEM);
 }
 
@@ -1144,7 +1146,6 @@ static tsf_status stage_bwd_public(tsf_handle* h, int axis, const tsf_bf16* q, c
   if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
   h->launches = 0;
   if (h->world != 1) return fail(h, TSF_ERR_UNSUPPORTED, "the backward runs on single-GPU handles");
-  if (h->d == 128) return fail(h, TSF_ERR_UNSUPPORTED, "the backward supports d in {32, 64}");
   const size_t E = (size_t)h->K * h->N * h->H * h->d;
   for (const void* o : {(const void*)dq, (const void*)dk, (const void*)dv}) {
     tsf_status s = check_ptrs(h, {q, k, v, dO}, o, E * 2, E * 2);
@@ -1192,7 +1193,6 @@ tsf_status tsf_spacetime_block_bwd(tsf_handle* h, const tsf_bf16* x, const float
   if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
   h->launches = 0;
   if (h->world != 1) return fail(h, TSF_ERR_UNSUPPORTED, "the backward runs on single-GPU handles");
-  if (h->d == 128) return fail(h, TSF_ERR_UNSUPPORTED, "the backward supports d in {32, 64}");
   const size_t E = (size_t)h->K * h->N * h->H * h->d;
   tsf_status s = check_ptrs(h, {x}, dx, E * 2, E * 4);
   if (s != TSF_OK) return s;

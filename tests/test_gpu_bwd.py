@@ -29,7 +29,8 @@ def check(got, want, what):
     assert np.all(np.isfinite(got)) and rel <= 2e-2 and err <= 3e-2 * ref, what
 
 
-SHAPES = [(4, 64, 2, 32), (8, 300, 2, 64), (200, 4, 2, 64), (3, 130, 1, 64), (1, 257, 2, 64), (130, 3, 2, 32)]
+SHAPES = [(4, 64, 2, 32), (8, 300, 2, 64), (200, 4, 2, 64), (3, 130, 1, 64), (1, 257, 2, 64), (130, 3, 2, 32),
+          (5, 260, 2, 128), (150, 4, 1, 128)]   # d = 128 (the C4 head dim): packed and key-tile paths
 
 
 @pytest.mark.parametrize("shape", SHAPES)
@@ -59,9 +60,11 @@ def test_block_bwd_matches_oracle(tsf_lib, shape):
     check(dx, oracle.block_bwd(synth.bf16_bits_to_f64(xb), dy.astype(np.float64)), f"block bwd {shape} dx")
 
 
-def test_bwd_rejects_d128(tsf_lib):
-    layer = tsf_lib.Layer(2, 64, 1, 128)
-    z = torch.zeros((2, 64, 1, 128), dtype=torch.bfloat16, device="cuda")
-    with pytest.raises(tsf_lib.TsfError) as e:
-        layer.attn_bwd(1, z, z, z, z)
-    assert e.value.status == tsf_lib.TSF_ERR_UNSUPPORTED
+def test_block_bwd_d128(tsf_lib):
+    K, N, H, d = 4, 200, 2, 128
+    xb = synth.make_x(K, N, H, d, seed=65)
+    dy = np.random.default_rng(66).normal(0.0, 1.0, (K, N, H, d)).astype(np.float32)
+    layer = tsf_lib.Layer(K, N, H, d)
+    dx = layer.block_bwd(synth.bits_to_torch(xb, "cuda"), torch.from_numpy(dy).cuda())
+    torch.cuda.synchronize()
+    check(dx, oracle.block_bwd(synth.bf16_bits_to_f64(xb), dy.astype(np.float64)), f"block bwd {(K, N, H, d)} dx")
