@@ -157,8 +157,12 @@ tsf_status tsf_temporal_attn_bwd(tsf_handle* h, const tsf_bf16* q, const tsf_bf1
 tsf_status tsf_spatial_attn_bwd(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v,
                                 const tsf_bf16* dO, tsf_bf16* dq, tsf_bf16* dk, tsf_bf16* dv, void* stream);
 
-/* Backward of tsf_spacetime_block: dx for x (bf16) and dy (fp32), both
- * [K, N, H, d]:  dX_t = dy + (dq + dk + dv of S at X_t),  dx = dX_t + (dq + dk +
+/* Backward of tsf_spacetime_block: dx (fp32) for x (bf16) and dy (fp32).
+ * Single GPU: all [K, N, H, d].  Distributed handle: x and dx are the rank's
+ * token shard [K, N/P, H, d], dy its frame shard [K/P, N, H, d], and the
+ * exchange runs in reverse (X_t token -> frame shard, then dX_t frame ->
+ * token shard as fp32 bytes); simulated handles take all shards stacked.
+ * Collective on distributed handles.  Gradient:   dX_t = dy + (dq + dk + dv of S at X_t),  dx = dX_t + (dq + dk +
  * dv of T at x)  (q = k = v in each stage).  X_t is recomputed in bf16 (the
  * training precision; the forward keeps it in fp16, reading G8), so dx
  * carries bf16-level error (tests: rel-L2 <= 1e-2).  dx fp32. */

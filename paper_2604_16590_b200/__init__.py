@@ -275,13 +275,14 @@ class Layer:
         return dq, dk, dv
 
     def block_bwd(self, x, dy, out=None, stream=None):
-        """tsf_spacetime_block_bwd: x bf16, dy fp32 -> dx fp32 (all [K, N, H, d])."""
+        """tsf_spacetime_block_bwd: x bf16 (token shard), dy fp32 (frame shard) -> dx fp32
+        (token shard); all [K, N, H, d] on one GPU.  Distributed / simulated handles run
+        the exchange reversed (frame -> token shard for dX_t)."""
         import torch
-        shp = (self.K, self.N, self.H, self.d)
-        _need(x, torch.bfloat16, shp, "x")
-        _need(dy, torch.float32, shp, "dy")
-        out = torch.empty(shp, dtype=torch.float32, device=x.device) if out is None else out
-        _need(out, torch.float32, shp, "out")
+        _need(x, torch.bfloat16, self.token_shard_shape, "x")
+        _need(dy, torch.float32, self.frame_shard_shape, "dy")
+        out = torch.empty(self.token_shard_shape, dtype=torch.float32, device=x.device) if out is None else out
+        _need(out, torch.float32, self.token_shard_shape, "out")
         _check(lib().tsf_spacetime_block_bwd(self._h, x.data_ptr(), dy.data_ptr(), out.data_ptr(), _stream_ptr(stream)),
                self._h)
         return out

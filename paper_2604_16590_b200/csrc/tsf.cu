@@ -1050,7 +1050,7 @@ static tsf_status stage_bwd(tsf_handle* h, const View& v, const void* q, const v
   const int d = h->d;
   const int nt = (v.L + 127) / 128;
   const int pitch = nt * 128;
-  const size_t E0 = (size_t)h->K * h->N * h->H * d;
+  const size_t E0 = (size_t)v.L * v.A * v.B * d;  // elements of the viewed (contiguous) tensor
   if (v.L <= 128) {
     // packed: G = 128 / L whole groups per tile, row statistics computed in the
     // kernel (no forward recompute), one launch
@@ -1102,8 +1102,7 @@ static tsf_status stage_bwd(tsf_handle* h, const View& v, const void* q, const v
   h->st_pitch = 0;
   if (s != TSF_OK) return s;
   // 2. the key-tile backward
-  const size_t E = (size_t)h->K * h->N * h->H * d;
-  TSF_CUDA(h, cudaMemsetAsync(dqacc, 0, E * sizeof(float), st));
+  TSF_CUDA(h, cudaMemsetAsync(dqacc, 0, E0 * sizeof(float), st));
   CUtensorMap mq, mk, mv, mdo;
   if ((s = make_map(h, &mq, q, d, v, 128, 1, 1, false)) != TSF_OK) return s;
   if ((s = make_map(h, &mk, k, d, v, 128, 1, 1, false)) != TSF_OK) return s;
@@ -1189,10 +1188,99 @@ tsf_status tsf_spatial_attn_bwd(tsf_handle* h, const tsf_bf16* q, const tsf_bf16
   return stage_bwd_public(h, 1, q, k, v, dO, dq, dk, dv, stream);
 }
 
+}  // extern "C"
+
+extern "C" {
+static tsf_status check_comm(tsf_handle* h);
+}
+static tsf_status reshard_gen(tsf_handle* h, int dir, const void* in, void* out, int elem_bytes, void* scratch,
+                              cudaStream_t st);
+
+// Distributed block backward (P > 1, real or simulated ranks), the exchange
+// reversed: x token shard -> X_t token shard (temporal forward, local) -> X_t
+// frame shard (T2S) -> spatial backward on the frame shard with dy -> dX_t
+// frame shard (fp32) -> dX_t token shard (S2T, fp32 bytes) -> temporal
+// backward on the token shard -> dx token shard.  Simulated handles take every
+// rank's shards stacked, as tsf_spacetime_block does.
+static tsf_status block_bwd_dist(tsf_handle* h, const tsf_bf16* x, const float* dy, float* dx, cudaStream_t st) {
+  const int P = h->world, Nl = h->N / P, Kl = h->K / P, H = h->H, d = h->d;
+  const int V = h->sim ? P : 1;
+  const size_t Es = (size_t)h->K * Nl * H * d;   // one rank's token shard = frame shard elements
+  const View vt = temporal_view(h->K, Nl, H, d), vs = spatial_view(Kl, h->N, H, d);
+  const size_t pt = (size_t)((vt.L + 127) / 128) * 128 * vt.A * vt.B, ps = (size_t)((vs.L + 127) / 128) * 128 * vs.A * vs.B;
+  const size_t pmax = pt > ps ? pt : ps;
+  // per handled rank: o_ws | xtb_tok | xtb_fr | dyb | dxtb | dk | dv (bf16) | dqacc | dxt_fr | dxt_tok | scratch (fp32)
+  const size_t per = 7 * Es * 2 + 4 * Es * 4;
+  const size_t need = V * per + 2 * pmax * 4 + 4096;
+  tsf_status s = bwd_workspace(h, need);
+  if (s != TSF_OK) return s;
+  char* base = static_cast<char*>(h->bw);
+  auto bfp = [&](int slot) { return reinterpret_cast<__nv_bfloat16*>(base + (size_t)slot * V * Es * 2); };
+  __nv_bfloat16 *o_ws = bfp(0), *xtb_tok = bfp(1), *xtb_fr = bfp(2), *dyb = bfp(3), *dxtb = bfp(4), *dk = bfp(5),
+                *dv = bfp(6);
+  float* f32 = reinterpret_cast<float*>(base + 7 * V * Es * 2);
+  float *dqacc = f32, *dxt_fr = f32 + V * Es, *dxt_tok = f32 + 2 * V * Es, *scratch = f32 + 3 * V * Es;
+  float* lse = f32 + 4 * V * Es;
+  float* drow = lse + pmax;
+  const long long n8 = (long long)(Es / 8);
+  const int g = ew_grid(h, n8);
+  // X_t token shard of every handled rank, then to frame shards
+  for (int r = 0; r < V; ++r) {
+    if ((s = run_attention(h, vt, x + r * Es, x + r * Es, x + r * Es, EPI_OUT16, o_ws + r * Es, nullptr, st)) != TSF_OK)
+      return s;
+    add_bf16_kernel<<<g, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(x) + r * Es, o_ws + r * Es,
+                                       xtb_tok + r * Es, n8);
+    h->launches++;
+  }
+  TSF_CUDA(h, cudaGetLastError());
+  if ((s = check_comm(h)) != TSF_OK) return s;
+  if ((s = reshard_gen(h, TSF_T2S, xtb_tok, xtb_fr, 2, scratch, st)) != TSF_OK) return s;
+  // spatial backward on each frame shard
+  for (int r = 0; r < V; ++r) {
+    f32_to_bf16_kernel<<<g, 256, 0, st>>>(dy + r * Es, dyb + r * Es, n8);
+    h->launches++;
+    const __nv_bfloat16* xf = xtb_fr + r * Es;
+    if ((s = stage_bwd(h, vs, xf, xf, xf, dyb + r * Es, dqacc + r * Es, dk + r * Es, dv + r * Es, o_ws + r * Es, lse,
+                       drow, st)) != TSF_OK)
+      return s;
+    sum4_kernel<<<g, 256, 0, st>>>(dy + r * Es, dqacc + r * Es, dk + r * Es, dv + r * Es, dxt_fr + r * Es, nullptr, n8);
+    h->launches++;
+  }
+  TSF_CUDA(h, cudaGetLastError());
+  // dX_t back to token shards (fp32 bytes, bit-exact)
+  if ((s = reshard_gen(h, TSF_S2T, dxt_fr, dxt_tok, 4, scratch, st)) != TSF_OK) return s;
+  // temporal backward on each token shard
+  for (int r = 0; r < V; ++r) {
+    f32_to_bf16_kernel<<<g, 256, 0, st>>>(dxt_tok + r * Es, dxtb + r * Es, n8);
+    h->launches++;
+    const tsf_bf16* xr = x + r * Es;
+    if ((s = stage_bwd(h, vt, xr, xr, xr, dxtb + r * Es, dqacc + r * Es, dk + r * Es, dv + r * Es, o_ws + r * Es, lse,
+                       drow, st)) != TSF_OK)
+      return s;
+    sum4_kernel<<<g, 256, 0, st>>>(dxt_tok + r * Es, dqacc + r * Es, dk + r * Es, dv + r * Es, dx + r * Es, nullptr, n8);
+    h->launches++;
+  }
+  TSF_CUDA(h, cudaGetLastError());
+  return TSF_OK;
+}
+
+extern "C" {
+
 tsf_status tsf_spacetime_block_bwd(tsf_handle* h, const tsf_bf16* x, const float* dy, float* dx, void* stream) {
   if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
   h->launches = 0;
-  if (h->world != 1) return fail(h, TSF_ERR_UNSUPPORTED, "the backward runs on single-GPU handles");
+  if (h->world != 1) {
+    const size_t Eall = (size_t)h->K * (h->N / h->world) * h->H * h->d * (h->sim ? h->world : 1);
+    tsf_status s = check_ptrs(h, {x}, dx, Eall * 2, Eall * 4);
+    if (s != TSF_OK) return s;
+    if ((s = check_ptrs(h, {dy}, dx, Eall * 4, Eall * 4)) != TSF_OK) return s;
+    if ((s = check_comm(h)) != TSF_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    StageTimer tm(h, st, 8);
+    s = block_bwd_dist(h, x, dy, dx, st);
+    tm.done();
+    return s;
+  }
   const size_t E = (size_t)h->K * h->N * h->H * h->d;
   tsf_status s = check_ptrs(h, {x}, dx, E * 2, E * 4);
   if (s != TSF_OK) return s;
@@ -1766,6 +1854,72 @@ tsf_status tsf_sync(tsf_handle* h, void* stream, int timeout_ms) {
   return TSF_OK;
 }
 
+}  // extern "C"
+
+// The exchange's byte plan for any element size: rank r's shard is shard_bytes;
+// its block p (peer_bytes) goes to rank p, which stores it at slot r.  Real
+// ranks: one grouped NCCL send/recv round on `st`; simulated ranks (stacked
+// shards): device copies.
+static tsf_status exchange_bytes(tsf_handle* h, const char* src, char* dst, size_t shard_bytes, size_t peer_bytes,
+                                 cudaStream_t st) {
+  const int P = h->world;
+  if (h->sim) {
+    for (int r = 0; r < P; ++r)
+      for (int p = 0; p < P; ++p)
+        TSF_CUDA(h, cudaMemcpyAsync(dst + p * shard_bytes + r * peer_bytes, src + r * shard_bytes + p * peer_bytes,
+                                    peer_bytes, cudaMemcpyDeviceToDevice, st));
+    return TSF_OK;
+  }
+  TSF_NCCL(h, ncclGroupStart());
+  for (int p = 0; p < P; ++p) {
+    TSF_NCCL(h, ncclSend(src + p * peer_bytes, peer_bytes, ncclUint8, p, h->comm, st));
+    TSF_NCCL(h, ncclRecv(dst + p * peer_bytes, peer_bytes, ncclUint8, p, h->comm, st));
+  }
+  TSF_NCCL(h, ncclGroupEnd());
+  return TSF_OK;
+}
+
+// Token shard <-> frame shard of a [K, N, H, d] tensor of elem_bytes-sized
+// elements (untyped, bit-exact).  scratch: one shard per rank handled.
+static tsf_status reshard_gen(tsf_handle* h, int dir, const void* in, void* out, int elem_bytes, void* scratch,
+                              cudaStream_t st) {
+  const int P = h->world, Kc = h->K / P, Nc = h->N / P;
+  const size_t shard = (size_t)h->K * Nc * h->H * h->d * elem_bytes, peer = shard / P;
+  const int vecs = h->H * h->d * elem_bytes / 16;
+  const long long items = (long long)P * Kc * Nc * vecs;
+  const int V = h->sim ? P : 1;
+  const char* cin = static_cast<const char*>(in);
+  char* cout = static_cast<char*>(out);
+  char* sc = static_cast<char*>(scratch);
+  tsf_status s;
+  if (dir == TSF_T2S) {
+    // send frames [p Kc, (p+1) Kc) of the token shard (contiguous); receive
+    // [P][Kc][Nc] blocks, unpack to [Kc][N]
+    if ((s = exchange_bytes(h, cin, sc, shard, peer, st)) != TSF_OK) return s;
+    for (int r = 0; r < V; ++r) {
+      reshard_perm_kernel<true><<<grid_for(h, items), 256, 0, st>>>((const uint4*)(sc + r * shard),
+                                                                    (uint4*)(cout + r * shard), nullptr, nullptr, P,
+                                                                    Kc, Nc, vecs);
+      h->launches++;
+    }
+  } else {
+    // pack [Kc][N] -> [P][Kc][Nc], send block p to peer p; the received
+    // blocks [P][Kc][Nc] are exactly the token shard [K][Nc]
+    for (int r = 0; r < V; ++r) {
+      reshard_perm_kernel<false><<<grid_for(h, items), 256, 0, st>>>((const uint4*)(cin + r * shard),
+                                                                     (uint4*)(sc + r * shard), nullptr, nullptr, P,
+                                                                     Kc, Nc, vecs);
+      h->launches++;
+    }
+    TSF_CUDA(h, cudaGetLastError());
+    if ((s = exchange_bytes(h, sc, cout, shard, peer, st)) != TSF_OK) return s;
+  }
+  TSF_CUDA(h, cudaGetLastError());
+  return TSF_OK;
+}
+
+extern "C" {
+
 tsf_status tsf_reshard(tsf_handle* h, int dir, const tsf_bf16* in, tsf_bf16* out, void* stream) {
   if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
   if (dir != TSF_T2S && dir != TSF_S2T) return fail(h, TSF_ERR_CONFIG, "bad direction");
@@ -1782,56 +1936,9 @@ tsf_status tsf_reshard(tsf_handle* h, int dir, const tsf_bf16* in, tsf_bf16* out
     tm.done();
     return TSF_OK;
   }
-  const size_t chunk = bytes / P;
-  const int vecs = h->H * h->d * 2 / 16;
-  const long long items = (long long)P * Kc * Nc * vecs;
-  const size_t El = bytes / 2;  // elements of one rank's shard
-  const __half* hin = reinterpret_cast<const __half*>(in);
-  __half* hout = reinterpret_cast<__half*>(out);
-  const int V = h->sim ? P : 1;  // ranks handled by this call
-  if (dir == TSF_T2S) {
-    // send frames [p Kc, (p+1) Kc) of the token shard (contiguous); receive
-    // [P][Kc][Nc] blocks, unpack to [Kc][N]
-    if (h->sim) {
-      if ((s = exchange_sim(h, hin, h->rxt, El, 0, 0, chunk, st)) != TSF_OK) return s;
-    } else {
-      TSF_NCCL(h, ncclGroupStart());
-      for (int p = 0; p < P; ++p) {
-        TSF_NCCL(h, ncclSend((const char*)in + p * chunk, chunk, ncclUint8, p, h->comm, st));
-        TSF_NCCL(h, ncclRecv((char*)h->rxt + p * chunk, chunk, ncclUint8, p, h->comm, st));
-      }
-      TSF_NCCL(h, ncclGroupEnd());
-    }
-    for (int r = 0; r < V; ++r) {
-      reshard_perm_kernel<true><<<grid_for(h, items), 256, 0, st>>>((const uint4*)(h->rxt + r * El),
-                                                                    (uint4*)(hout + r * El), nullptr, nullptr, P,
-                                                                    Kc, Nc, vecs);
-      h->launches++;
-    }
-  } else {
-    // pack [Kc][N] -> [P][Kc][Nc], send block p to peer p; the received
-    // blocks [P][Kc][Nc] are exactly the token shard [K][Nc]
-    for (int r = 0; r < V; ++r) {
-      reshard_perm_kernel<false><<<grid_for(h, items), 256, 0, st>>>((const uint4*)(hin + r * El),
-                                                                     (uint4*)(h->rxt + r * El), nullptr, nullptr,
-                                                                     P, Kc, Nc, vecs);
-      h->launches++;
-    }
-    TSF_CUDA(h, cudaGetLastError());
-    if (h->sim) {
-      if ((s = exchange_sim(h, h->rxt, hout, El, 0, 0, chunk, st)) != TSF_OK) return s;
-    } else {
-      TSF_NCCL(h, ncclGroupStart());
-      for (int p = 0; p < P; ++p) {
-        TSF_NCCL(h, ncclSend((const char*)h->rxt + p * chunk, chunk, ncclUint8, p, h->comm, st));
-        TSF_NCCL(h, ncclRecv((char*)out + p * chunk, chunk, ncclUint8, p, h->comm, st));
-      }
-      TSF_NCCL(h, ncclGroupEnd());
-    }
-  }
-  TSF_CUDA(h, cudaGetLastError());
+  s = reshard_gen(h, dir, in, out, 2, h->rxt, st);
   tm.done();
-  return TSF_OK;
+  return s;
 }
 
 #ifdef TSF_TRACE

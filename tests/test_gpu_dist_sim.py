@@ -109,3 +109,29 @@ def test_sim_handle_rejects_bad_world(tsf_lib):
     with pytest.raises(tsf_lib.TsfError) as e:
         tsf_lib.Layer(8, 64, 2, 64, sim_world=16)     # beyond the 8 GPUs of a box
     assert e.value.status == tsf_lib.TSF_ERR_CONFIG
+
+
+@pytest.mark.parametrize("P,shape", [(2, (8, 256, 2, 64)), (4, (8, 256, 2, 64)), (4, (200, 16, 2, 64)),
+                                     (2, (4, 128, 2, 128))])
+def test_sim_block_bwd_equals_single_gpu(tsf_lib, P, shape):
+    """NEXT-2, the exchange reversed: the P-rank block backward (dX_t frame shard ->
+    token shard as fp32 bytes) gives dx bitwise equal to the single-GPU backward,
+    and matches the fp64 oracle."""
+    K, N, H, d = shape
+    Nl, Kl = N // P, K // P
+    xb = synth.make_x(K, N, H, d, seed=71)
+    dy = np.random.default_rng(72).normal(0.0, 1.0, (K, N, H, d)).astype(np.float32)
+    one = tsf_lib.Layer(K, N, H, d)
+    dx1 = one.block_bwd(synth.bits_to_torch(xb, "cuda"), torch.from_numpy(dy).cuda()).cpu()
+    sim = tsf_lib.Layer(K, N, H, d, sim_world=P, sim_mode=1)
+    xs = synth.bits_to_torch(stack_token_shards(xb, P), "cuda")
+    dys = torch.from_numpy(np.ascontiguousarray(dy)).reshape(P, Kl, N, H, d).cuda()   # frame shards stacked
+    dxs = sim.block_bwd(xs, dys)
+    sim.sync()
+    dx = torch.cat([dxs[r] for r in range(P)], dim=1).cpu()        # token shards -> [K, N, H, d]
+    assert torch.equal(dx, dx1), f"P={P}: max |ddx| {(dx - dx1).abs().max().item():.3e} (must be bitwise equal)"
+    want = oracle.block_bwd(synth.bf16_bits_to_f64(xb), dy.astype(np.float64))
+    rel = np.linalg.norm(dx.double().numpy() - want) / np.linalg.norm(want)
+    assert rel <= 2e-2
+    one.close()
+    sim.close()
