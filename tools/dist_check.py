@@ -5,7 +5,8 @@
 Each rank: x token shard -> tsf_spacetime_block -> y frame shard, compared with
 the fp64 oracle on sampled rows + a full plane of the rank's frames; the
 reshard round trip must be bit-exact; y on P GPUs must equal the single-GPU
-y bitwise (same kernel tiles per group).
+y bitwise (same kernel tiles per group), and so must the backward's dx (the
+exchange reversed).
 """
 import os
 import sys
@@ -64,18 +65,27 @@ def main():
     exact_fr = torch.equal(fr.cpu(), synth.bits_to_torch(np.ascontiguousarray(xb_full[rank * Kl:(rank + 1) * Kl])))
     exact_back = torch.equal(back, xs)
 
+    # backward (NEXT-2), the exchange reversed: dy frame shard -> dx token shard
+    dy_full = np.random.default_rng(99).normal(0.0, 1.0, (K, N, H, d)).astype(np.float32)
+    dys = torch.from_numpy(np.ascontiguousarray(dy_full[rank * Kl:(rank + 1) * Kl])).cuda()
+    dx = layer.block_bwd(xs, dys) if d in (32, 64, 128) else None
+    torch.cuda.synchronize()
+
     # bitwise equality with the single-GPU result (rank 0 computes the full layer)
-    same = None
+    same = same_bwd = None
     if rank == 0:
         single = tsf.Layer(K, N, H, d)
         y1 = single.block(synth.bits_to_torch(xb_full, "cuda"))
+        dx1 = single.block_bwd(synth.bits_to_torch(xb_full, "cuda"), torch.from_numpy(dy_full).cuda())
         torch.cuda.synchronize()
         same = torch.equal(y1[:Kl], y)
+        same_bwd = torch.equal(dx1[:, :Nl], dx)
         single.close()
     print(f"rank {rank}/{world}: block sampled max-abs {err:.3e}, plane max-abs {perr:.3e}, "
           f"t2s exact {exact_fr}, round trip exact {exact_back}, back-to-back bitwise {b2b}, "
-          f"equals single-GPU bitwise {same}", flush=True)
-    ok = err <= 2e-2 and perr <= 2e-2 and exact_fr and exact_back and b2b and (same in (None, True))
+          f"equals single-GPU bitwise {same}, backward equals single-GPU bitwise {same_bwd}", flush=True)
+    ok = (err <= 2e-2 and perr <= 2e-2 and exact_fr and exact_back and b2b and (same in (None, True))
+          and (same_bwd in (None, True)))
     flag = torch.tensor([0 if ok else 1], device="cuda")
     dist.all_reduce(flag)
     layer.close()
