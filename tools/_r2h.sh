@@ -1,4 +1,4 @@
-O=gpurun_out/r2h; mkdir -p $O
+O=gpurun_out/${TAG:-r2h}; mkdir -p $O
 nvidia-smi -L > $O/gpus.txt; NG=$(nvidia-smi -L | wc -l); echo "GPUs: $NG"
 timeout 300 python bench.py --steps 500 --warmup 10 --no-cpu-baseline > $O/scale_1.json 2> $O/scale_1.err; echo "P=1 rc=$?"
 for P in 2 4; do
@@ -13,7 +13,7 @@ python - <<'PY'
 import json
 for P in (1, 2, 4):
     try:
-        d = json.loads(open(f"gpurun_out/r2h/scale_{P}.json").read().strip().splitlines()[-1])
+        d = json.loads(open(f"gpurun_out/${TAG:-r2h}/scale_{P}.json").read().strip().splitlines()[-1])
         print(P, round(d["value"] / 1e6, 2), "Mtok/s", round(d["ms_per_step"], 4), "ms/step", d.get("a2a", {}).get("exchange_GBs_per_rank"), d["clocks"]["sm_mhz"], d["clocks"]["reasons"])
     except Exception as e:
         print(P, "no line", e)
