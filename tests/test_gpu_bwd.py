@@ -68,3 +68,14 @@ def test_block_bwd_d128(tsf_lib):
     dx = layer.block_bwd(synth.bits_to_torch(xb, "cuda"), torch.from_numpy(dy).cuda())
     torch.cuda.synchronize()
     check(dx, oracle.block_bwd(synth.bf16_bits_to_f64(xb), dy.astype(np.float64)), f"block bwd {(K, N, H, d)} dx")
+
+
+def test_block_bwd_c2_shape(tsf_lib):
+    """C2's frame size and context (K = 8, N = 4096, d = 64) at 4 heads, every element."""
+    K, N, H, d = 8, 4096, 4, 64
+    xb = synth.make_x(K, N, H, d, seed=67)
+    dy = np.random.default_rng(68).normal(0.0, 1.0, (K, N, H, d)).astype(np.float32)
+    layer = tsf_lib.Layer(K, N, H, d)
+    dx = layer.block_bwd(synth.bits_to_torch(xb, "cuda"), torch.from_numpy(dy).cuda())
+    torch.cuda.synchronize()
+    check(dx, oracle.block_bwd(synth.bf16_bits_to_f64(xb), dy.astype(np.float64)), f"block bwd {(K, N, H, d)} dx")

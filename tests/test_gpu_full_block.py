@@ -66,3 +66,20 @@ def test_full_block_rejects_unsupported_width(tsf_lib):
     with pytest.raises(tsf_lib.TsfError) as e:
         layer.full_block(torch.zeros((2, 64, 1, 32), dtype=torch.bfloat16, device="cuda"), params)
     assert e.value.status == tsf_lib.TSF_ERR_UNSUPPORTED
+
+
+def test_full_block_c2_size(tsf_lib):
+    """The bench workload's shape (BASELINE configs[1]: K=8, N=4096, H=16, d=64) with
+    D = 1024 and a 4D MLP, every output element against the oracle."""
+    K, N, H, d, F = 8, 4096, 16, 64, 4096
+    xb = synth.make_x(K, N, H, d, seed=55)
+    params = synth.make_block_params(H, d, F, seed=56)
+    layer = tsf_lib.Layer(K, N, H, d)
+    y = layer.full_block(synth.bits_to_torch(xb, "cuda"), dev_params(params))
+    torch.cuda.synchronize()
+    got = y.double().cpu().numpy()
+    want = oracle.full_block(synth.bf16_bits_to_f64(xb), synth.block_params_f64(params))
+    err = np.abs(got - want).max()
+    rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+    print(f"full block C2 F={F}: max-abs {err:.3e} rel-L2 {rel:.3e} max|ref| {np.abs(want).max():.2f}")
+    assert np.all(np.isfinite(got)) and rel <= 1e-2 and err <= 5e-2
