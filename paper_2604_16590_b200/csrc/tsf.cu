@@ -396,8 +396,10 @@ template <int D, int WIN>
 static tsf_status launch_stream_t(tsf_handle* h, cudaStream_t st, const CUtensorMap& mx, const CUtensorMap& mo,
                                   const AttnParams& p) {
   if constexpr (D <= 64 && WIN <= 64) {
-    if (stream_slots() == 2) return launch_stream_ns<D, WIN, 2>(h, st, mx, mo, p);
-    return launch_stream_ns<D, WIN, 4>(h, st, mx, mo, p);
+    if constexpr (D == 64) {  // the four-slot A/B variant is built for d = 64 only
+      if (stream_slots() == 4) return launch_stream_ns<D, WIN, 4>(h, st, mx, mo, p);
+    }
+    return launch_stream_ns<D, WIN, 2>(h, st, mx, mo, p);
   }
   return fail(h, TSF_ERR_UNSUPPORTED, "stream kernel shape");
 }
@@ -450,15 +452,6 @@ static bool use_flash3(int d, int epi) {
   }
   return env != 0 && d == 64 && (epi == EPI_BLOCK_S || epi == EPI_OUT16);
 }
-static int flash3_emu() {
-  static int env = -2;
-  if (env == -2) {
-    const char* e = getenv("TSF_EMU3");
-    env = e ? atoi(e) : 4;
-  }
-  return env;
-}
-
 static int flash3_cps() {  // CTAs per SM (TSF_F3CTAS: 3 | 4)
   static int env = -2;
   if (env == -2) {
@@ -483,21 +476,12 @@ static tsf_status launch_flash3_cps(tsf_handle* h, cudaStream_t st, const CUtens
                 st, pp, mq, mk, mv);
 }
 
-template <int EPI, int EMU>
-static tsf_status launch_flash3_emu(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
-                                    const CUtensorMap& mv, const AttnParams& p) {
-  if (flash3_cps() == 4) return launch_flash3_cps<EPI, EMU, 4>(h, st, mq, mk, mv, p);
-  return launch_flash3_cps<EPI, EMU, 3>(h, st, mq, mk, mv, p);
-}
-
+// flash3 is an A/B variant (off by default): one exp split (EMU = 4), 3 or 4 CTAs per SM
 template <int EPI>
 static tsf_status launch_flash3(tsf_handle* h, cudaStream_t st, const CUtensorMap& mq, const CUtensorMap& mk,
                                 const CUtensorMap& mv, const AttnParams& p) {
-  switch (flash3_emu()) {
-    case 0: return launch_flash3_emu<EPI, 0>(h, st, mq, mk, mv, p);
-    case 6: return launch_flash3_emu<EPI, 6>(h, st, mq, mk, mv, p);
-    default: return launch_flash3_emu<EPI, 4>(h, st, mq, mk, mv, p);
-  }
+  if (flash3_cps() == 4) return launch_flash3_cps<EPI, 4, 4>(h, st, mq, mk, mv, p);
+  return launch_flash3_cps<EPI, 4, 3>(h, st, mq, mk, mv, p);
 }
 
 // Flash kernel with fixed tile / exp settings for the secondary calls: joint
