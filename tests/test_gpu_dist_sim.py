@@ -115,8 +115,10 @@ def test_sim_handle_rejects_bad_world(tsf_lib):
                                      (2, (4, 128, 2, 128))])
 def test_sim_block_bwd_equals_single_gpu(tsf_lib, P, shape):
     """NEXT-2, the exchange reversed: the P-rank block backward (dX_t frame shard ->
-    token shard as fp32 bytes) gives dx bitwise equal to the single-GPU backward,
-    and matches the fp64 oracle."""
+    token shard as fp32 bytes) matches the single-GPU backward and the fp64 oracle.
+    Not bitwise: dq is accumulated with fp32 atomic reductions across key tiles,
+    whose order varies (G22); the exchanges themselves are bit-exact
+    (test_sim_reshard_is_the_index_permutation)."""
     K, N, H, d = shape
     Nl, Kl = N // P, K // P
     xb = synth.make_x(K, N, H, d, seed=71)
@@ -129,7 +131,9 @@ def test_sim_block_bwd_equals_single_gpu(tsf_lib, P, shape):
     dxs = sim.block_bwd(xs, dys)
     sim.sync()
     dx = torch.cat([dxs[r] for r in range(P)], dim=1).cpu()        # token shards -> [K, N, H, d]
-    assert torch.equal(dx, dx1), f"P={P}: max |ddx| {(dx - dx1).abs().max().item():.3e} (must be bitwise equal)"
+    diff = (dx.double() - dx1.double())
+    assert diff.norm() <= 1e-4 * dx1.double().norm() and diff.abs().max() <= 1e-2 * dx1.abs().max(), \
+        f"P={P}: max |ddx| {diff.abs().max().item():.3e}"
     want = oracle.block_bwd(synth.bf16_bits_to_f64(xb), dy.astype(np.float64))
     rel = np.linalg.norm(dx.double().numpy() - want) / np.linalg.norm(want)
     assert rel <= 2e-2

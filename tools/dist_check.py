@@ -5,8 +5,9 @@
 Each rank: x token shard -> tsf_spacetime_block -> y frame shard, compared with
 the fp64 oracle on sampled rows + a full plane of the rank's frames; the
 reshard round trip must be bit-exact; y on P GPUs must equal the single-GPU
-y bitwise (same kernel tiles per group), and so must the backward's dx (the
-exchange reversed).
+y bitwise (same kernel tiles per group); the backward's dx (the exchange
+reversed) must match the single-GPU dx within rel-L2 1e-4 (its dq is
+accumulated with fp32 atomics, so it is not bitwise reproducible).
 """
 import os
 import sys
@@ -79,11 +80,15 @@ def main():
         dx1 = single.block_bwd(synth.bits_to_torch(xb_full, "cuda"), torch.from_numpy(dy_full).cuda())
         torch.cuda.synchronize()
         same = torch.equal(y1[:Kl], y)
-        same_bwd = torch.equal(dx1[:, :Nl], dx)
+        # the backward's dq is accumulated with fp32 atomic reductions across key
+        # tiles (order-dependent rounding), so dx is compared within a tolerance
+        ref = dx1[:, :Nl].double()
+        diff = (dx.double() - ref)
+        same_bwd = bool(diff.norm() <= 1e-4 * ref.norm() and diff.abs().max() <= 1e-2 * ref.abs().max())
         single.close()
     print(f"rank {rank}/{world}: block sampled max-abs {err:.3e}, plane max-abs {perr:.3e}, "
           f"t2s exact {exact_fr}, round trip exact {exact_back}, back-to-back bitwise {b2b}, "
-          f"equals single-GPU bitwise {same}, backward equals single-GPU bitwise {same_bwd}", flush=True)
+          f"equals single-GPU bitwise {same}, backward matches single-GPU (rel-L2 <= 1e-4) {same_bwd}", flush=True)
     ok = (err <= 2e-2 and perr <= 2e-2 and exact_fr and exact_back and b2b and (same in (None, True))
           and (same_bwd in (None, True)))
     flag = torch.tensor([0 if ok else 1], device="cuda")
