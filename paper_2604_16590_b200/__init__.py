@@ -265,7 +265,7 @@ class Layer:
     def attn_bwd(self, axis: int, q, k, v, dO, stream=None):
         """tsf_temporal_attn_bwd (axis 0) / tsf_spatial_attn_bwd (axis 1): (dq, dk, dv) bf16."""
         import torch
-        shp = (self.K, self.N, self.H, self.d)
+        shp = (self.token_shard_shape if axis == 0 else self.frame_shard_shape)[-4:]
         for t, n in ((q, "q"), (k, "k"), (v, "v"), (dO, "dO")):
             _need(t, torch.bfloat16, shp, n)
         dq, dk, dv = (torch.empty_like(q) for _ in range(3))

@@ -1128,15 +1128,18 @@ static tsf_status stage_bwd_public(tsf_handle* h, int axis, const tsf_bf16* q, c
                                    const tsf_bf16* dO, tsf_bf16* dq, tsf_bf16* dk, tsf_bf16* dv, void* stream) {
   if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
   h->launches = 0;
-  if (h->world != 1) return fail(h, TSF_ERR_UNSUPPORTED, "the backward runs on single-GPU handles");
-  const size_t E = (size_t)h->K * h->N * h->H * h->d;
+  // distributed (and simulated) handles: the rank's own shard, like the forward
+  // stage calls -- temporal on the token shard [K, N/P, H, d], spatial on the
+  // frame shard [K/P, N, H, d]; both are local (no exchange)
+  const int Nl = h->N / h->world, Kl = h->K / h->world;
+  const size_t E = (size_t)(axis == 0 ? h->K : Kl) * (axis == 0 ? Nl : h->N) * h->H * h->d;
   for (const void* o : {(const void*)dq, (const void*)dk, (const void*)dv}) {
     tsf_status s = check_ptrs(h, {q, k, v, dO}, o, E * 2, E * 2);
     if (s != TSF_OK) return s;
   }
   if (overlap(dq, E * 2, dk, E * 2) || overlap(dq, E * 2, dv, E * 2) || overlap(dk, E * 2, dv, E * 2))
     return fail(h, TSF_ERR_CONFIG, "gradient outputs overlap");
-  const View vw = axis == 0 ? temporal_view(h->K, h->N, h->H, h->d) : spatial_view(h->K, h->N, h->H, h->d);
+  const View vw = axis == 0 ? temporal_view(h->K, Nl, h->H, h->d) : spatial_view(Kl, h->N, h->H, h->d);
   const size_t groups = (size_t)vw.A * vw.B, pitch = (size_t)((vw.L + 127) / 128) * 128;
   const size_t need = E * 2 + E * 4 + 2 * groups * pitch * 4 + 1024;
   tsf_status s = bwd_workspace(h, need);

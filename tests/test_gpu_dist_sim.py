@@ -139,3 +139,16 @@ def test_sim_block_bwd_equals_single_gpu(tsf_lib, P, shape):
     assert rel <= 2e-2
     one.close()
     sim.close()
+
+
+def test_stage_bwd_on_a_shard_handle(tsf_lib):
+    """The stage backward calls on a (simulated) distributed handle act on one shard."""
+    K, N, H, d, P = 8, 256, 2, 64, 4
+    sim = tsf_lib.Layer(K, N, H, d, sim_world=P)
+    one = tsf_lib.Layer(K // P, N, H, d)
+    q, k, v, do = (synth.bits_to_torch(synth.make_iid(K // P, N, H, d, seed=s), "cuda") for s in (81, 82, 83, 84))
+    a = sim.attn_bwd(1, q, k, v, do)
+    b = one.attn_bwd(1, q, k, v, do)
+    torch.cuda.synchronize()
+    for x, y in zip(a, b):
+        assert (x.float() - y.float()).abs().max().item() <= 1e-2 * y.float().abs().max().item()
