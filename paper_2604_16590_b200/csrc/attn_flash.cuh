@@ -763,16 +763,19 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       };
       static_assert((SUB * 2 * D / 16 / 32) % 8 == 0, "conversion batching");
       int g = 0;
+      const bool skip = (p.flags & FLASH_NO_CONVERT) != 0;  // diagnostics: timing only, wrong results
       for (int k = 0; k < my_items; ++k) {
         const int qs = k % C::QST;
         mbar_wait(&q_full[qs], (k / C::QST) & 1);
-        convert_tile(sQ + qs * C::Q_BYTES, 128);
-        convert_tile(sQ + qs * C::Q_BYTES + C::Q_TILE, 128);
+        if (!skip) {
+          convert_tile(sQ + qs * C::Q_BYTES, 128);
+          convert_tile(sQ + qs * C::Q_BYTES + C::Q_TILE, 128);
+        }
         if (lane == 0) mbar_arrive(&q_conv[qs]);
         for (int j = 0; j < nkv; ++j, ++g) {
           const int s = g % NST;
           mbar_wait(&k_full[s], (g / NST) & 1);
-          convert_tile(sKV + s * C::STAGE_BYTES, SUB);
+          if (!skip) convert_tile(sKV + s * C::STAGE_BYTES, SUB);
           if (lane == 0) mbar_arrive(&kv_conv[s]);
         }
       }
