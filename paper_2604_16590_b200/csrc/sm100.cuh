@@ -150,6 +150,19 @@ TSF_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Non-blocking test: has the phase with the given parity completed?
+TSF_DEV bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
 // Producer-side wait: try_wait with a suspend-time hint, so a waiting TMA/MMA
 // warp sleeps until the phase completes instead of spinning on issue slots
 // the softmax warps of its sub-partition need.
