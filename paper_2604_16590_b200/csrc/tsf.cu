@@ -363,7 +363,7 @@ static bool use_stream(int d, int win) {
 }
 
 // TMEM slots of the stream kernel: TSF_STREAM_SLOTS = 2 | 4.  Four slots (S, P, O
-// aliased in 128 columns) measured no faster at C2 (34.7 vs 34.3 us, tools/_r2m.sh,
+// aliased in 128 columns) measured no faster at C2 (34.7 vs 34.3 us, profiles/r07/traces,
 // trace 1831 vs 1773 cycles per tile): the stage is not limited by tiles in flight.
 static int stream_slots() {
   static int env = -2;
