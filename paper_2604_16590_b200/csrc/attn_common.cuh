@@ -188,6 +188,12 @@ __device__ __forceinline__ uint32_t epilogue_row(const AttnParams& p, const floa
   constexpr bool F16 = EpiTraits<EPI>::F16;
   uint32_t nf = 0;
   off += 8 * u0;
+  // residual units loaded before any store (generic pointers: see epilogue_row_stage)
+  uint4 res[NU];
+  if constexpr (EPI != EPI_OUT16 && EPI != EPI_STORM_S) {
+#pragma unroll
+    for (int u = 0; u < NU; ++u) res[u] = tile_row_u4<D, ROWS>(res_tile, r, u0 + u);
+  }
 #pragma unroll
   for (int u = 0; u < NU; ++u) {
     float v[8];
@@ -209,7 +215,7 @@ __device__ __forceinline__ uint32_t epilogue_row(const AttnParams& p, const floa
       yp[0] = y0;
       yp[1] = y1;
     } else {
-      const uint4 rr = tile_row_u4<D, ROWS>(res_tile, r, u0 + u);
+      const uint4 rr = res[u];
       const float2 x0 = unpack2<F16>(rr.x), x1 = unpack2<F16>(rr.y), x2 = unpack2<F16>(rr.z),
                    x3 = unpack2<F16>(rr.w);
       if constexpr (EPI == EPI_STORM_X) {  // y = u + g O/l
@@ -343,9 +349,18 @@ __device__ __forceinline__ uint32_t epilogue_row_stage(const float* o_acc, float
   constexpr int SWB = (2 * D < 128) ? 2 * D : 128;
   constexpr int UPC = SWB / 16;
   uint32_t nf = 0;
+  // residual units are loaded four at a time before their stores: the tiles are
+  // reached through generic pointers, so a load after a store could not be
+  // hoisted by the compiler (four keeps the register footprint small)
+  constexpr int GU = (D / 8 < 4) ? D / 8 : 4;
+  uint4 res[GU];
 #pragma unroll
   for (int u = 0; u < D / 8; ++u) {
-    const uint4 rr = tile_row_u4<D, ROWS_IN>(res_tile, r, u);
+    if (u % GU == 0) {
+#pragma unroll
+      for (int e = 0; e < GU; ++e) res[e] = tile_row_u4<D, ROWS_IN>(res_tile, r, u + e);
+    }
+    const uint4 rr = res[u % GU];
     float v[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[i] = o_acc[8 * u + i] * inv_l;
