@@ -191,6 +191,20 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
  * the result is bitwise the device call's. */
 tsf_status tsf_spacetime_block_host(tsf_handle* h, const tsf_bf16* x_host, float* y_host, void* stream);
 
+/* n independent blocks from HOST buffers: y_host[i] = block(x_host[i]) for
+ * i < n, each pair shaped as in tsf_spacetime_block_host (pinned memory
+ * needed for overlap).  Pipelined through two device staging slots (allocated
+ * on first use, 2 x (x + y) bytes): the host->device copy of x_{i+1}, the
+ * block of item i and the device->host copy of y_i run concurrently (separate
+ * copy streams, one per PCIe direction), so a batch costs about
+ * max(H2D, D2H) per item instead of their sum.  Returns after `stream` has
+ * synchronised (all y_host written); host buffers must stay valid until then.
+ * Each y_host[i] is bitwise what tsf_spacetime_block_host gives for
+ * x_host[i].  n = 0 is a no-op; a null array or element is TSF_ERR_CONFIG.
+ * Collective on distributed handles (every rank passes the same n). */
+tsf_status tsf_spacetime_block_host_batch(tsf_handle* h, const tsf_bf16* const* x_host, float* const* y_host, int n,
+                                          void* stream);
+
 /* Wait for `stream` and report what the asynchronous work found:
  *   TSF_ERR_NUMERIC  a block since the last tsf_sync stored a non-finite X_t
  *                    (the flag is cleared);

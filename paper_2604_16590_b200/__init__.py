@@ -47,6 +47,7 @@ SIGNATURES = [
     ("tsf_spacetime_block_bwd", _I, [_P, _P, _P, _P, _P]),
     ("tsf_spacetime_block", _I, [_P, _P, _P, _P]),
     ("tsf_spacetime_block_host", _I, [_P, _P, _P, _P]),
+    ("tsf_spacetime_block_host_batch", _I, [_P, _P, _P, _I, _P]),
     ("tsf_destroy", None, [_P]),
     ("tsf_get_unique_id", _I, [_P]),
     ("tsf_create_dist", _I, [_I, _I, _I, _I, _P, _I, _I, ctypes.POINTER(_P)]),
@@ -306,6 +307,23 @@ class Layer:
         _check(lib().tsf_spacetime_block_host(self._h, x_host.data_ptr(), y_host.data_ptr(), _stream_ptr(stream)),
                self._h)
         return y_host
+
+    def block_host_batch(self, xs_host, ys_host, stream=None):
+        """tsf_spacetime_block_host_batch: lists of CPU (pinned) bf16 x / fp32 y tensors,
+        n independent blocks with H2D, compute and D2H pipelined."""
+        import torch
+        if len(xs_host) != len(ys_host):
+            raise ValueError("xs_host and ys_host differ in length")
+        for x, y in zip(xs_host, ys_host):
+            _need(x, torch.bfloat16, self.token_shard_shape, "x_host")
+            _need(y, torch.float32, self.frame_shard_shape, "y_host")
+            if x.is_cuda or y.is_cuda:
+                raise ValueError("block_host_batch takes host tensors")
+        n = len(xs_host)
+        xa = (_P * max(n, 1))(*[x.data_ptr() for x in xs_host])
+        ya = (_P * max(n, 1))(*[y.data_ptr() for y in ys_host])
+        _check(lib().tsf_spacetime_block_host_batch(self._h, xa, ya, n, _stream_ptr(stream)), self._h)
+        return ys_host
 
     def reshard(self, x, direction: int, out=None, stream=None):
         """tsf_reshard: TSF_T2S token shard -> frame shard, TSF_S2T the inverse (bit-exact)."""

@@ -42,8 +42,10 @@ struct tsf_handle {
   __half* xt = nullptr;    // X_t = x + T(x) in fp16, [K, N/P, H, d]
   __half* rxt = nullptr;   // dist: all-to-all receive [P][K/P][N/P][H][d] (also reshard scratch)
   __half* uxt = nullptr;   // dist: unpacked frame shard [K/P][N][H][d]
-  __nv_bfloat16* xdev = nullptr;                 // host API staging
+  __nv_bfloat16* xdev = nullptr;                 // host API staging, slot 0
   float* ydev = nullptr;
+  __nv_bfloat16* xdev2 = nullptr;                // slot 1 (tsf_spacetime_block_host_batch, n >= 2)
+  float* ydev2 = nullptr;
   std::string err;
   int launches = 0;
   bool timing = false;
@@ -71,8 +73,9 @@ struct tsf_handle {
   bool use_pm = false;
   // host API (single GPU): the spatial stage runs in frame chunks and each
   // chunk's y copy to the host overlaps the next chunk's compute
-  cudaStream_t copy_stream = nullptr;
-  std::vector<cudaEvent_t> ev_h;         // [HOST_CHUNKS + 1]
+  cudaStream_t copy_stream = nullptr;     // device -> host
+  cudaStream_t h2d_stream = nullptr;      // host -> device
+  std::vector<cudaEvent_t> ev_h;         // [HOST_CHUNKS + 1 + 6]: chunk ends, D2H end, per slot: x in, x used, y out
   // small device scratch allocated before the (collective) communicator init:
   // [0] 1-int all-reduce barrier, [16] agreement flag, [256..] IPC handle all-gather
   char* scratch = nullptr;
@@ -695,13 +698,13 @@ static tsf_status alloc_workspace(tsf_handle* h) {
 }
 
 static void free_workspace(tsf_handle* h) {
-  for (void* p : {(void*)h->xt, (void*)h->rxt, (void*)h->uxt, (void*)h->xdev, (void*)h->ydev, (void*)h->scratch,
-                  h->fb, h->bw})
+  for (void* p : {(void*)h->xt, (void*)h->rxt, (void*)h->uxt, (void*)h->xdev, (void*)h->ydev, (void*)h->xdev2,
+                  (void*)h->ydev2, (void*)h->scratch, h->fb, h->bw})
     if (p) cudaFree(p);
   if (h->nf_host) cudaFreeHost(const_cast<unsigned int*>(h->nf_host));
   h->xt = h->rxt = h->uxt = nullptr;
-  h->xdev = nullptr;
-  h->ydev = nullptr;
+  h->xdev = h->xdev2 = nullptr;
+  h->ydev = h->ydev2 = nullptr;
   h->scratch = nullptr;
   h->nf_host = nullptr;
   h->fb = nullptr;
@@ -889,6 +892,7 @@ void tsf_destroy(tsf_handle* h) {
   if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
   for (auto e : h->ev_h) cudaEventDestroy(e);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  if (h->h2d_stream) cudaStreamDestroy(h->h2d_stream);
   for (auto e : h->event_pool) cudaEventDestroy(e);
   free_workspace(h);
   if (h->trace) cudaFree(h->trace);
@@ -1736,77 +1740,121 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
   return TSF_OK;
 }
 
-tsf_status tsf_spacetime_block_host(tsf_handle* h, const tsf_bf16* x_host, float* y_host, void* stream) {
+// one staging slot (device x, y) of the host calls: both or neither allocated
+static tsf_status host_slot(tsf_handle* h, __nv_bfloat16** x, float** y, size_t in_bytes, size_t out_bytes) {
+  if (*x && *y) return TSF_OK;
+  if (!*x && cudaMalloc(x, in_bytes) != cudaSuccess) *x = nullptr;
+  if (*x && !*y && cudaMalloc(y, out_bytes) != cudaSuccess) *y = nullptr;
+  if (!*x || !*y) {  // a half-done allocation is undone
+    if (*x) cudaFree(*x);
+    *x = nullptr;
+    cudaGetLastError();
+    return fail(h, TSF_ERR_NOMEM, "staging cudaMalloc failed");
+  }
+  return TSF_OK;
+}
+
+tsf_status tsf_spacetime_block_host_batch(tsf_handle* h, const tsf_bf16* const* x_host, float* const* y_host, int n,
+                                          void* stream) {
   if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
-  if (!x_host || !y_host) return fail(h, TSF_ERR_CONFIG, "null host buffer");
+  if (n < 0 || (n > 0 && (!x_host || !y_host))) return fail(h, TSF_ERR_CONFIG, "need n >= 0 and pointer arrays");
+  for (int i = 0; i < n; ++i)
+    if (!x_host[i] || !y_host[i]) return fail(h, TSF_ERR_CONFIG, "null host buffer");
+  if (n == 0) return TSF_OK;
   const int P = h->world, Nl = h->N / P, Kl = h->K / P;
   const int V = h->sim ? P : 1;
   const size_t in_bytes = (size_t)h->K * Nl * h->H * h->d * 2 * V;
   const size_t out_bytes = (size_t)Kl * h->N * h->H * h->d * 4 * V;
-  if (!h->xdev || !h->ydev) {  // both or neither: a half-done allocation is undone
-    if (!h->xdev && cudaMalloc(&h->xdev, in_bytes) != cudaSuccess) h->xdev = nullptr;
-    if (h->xdev && !h->ydev && cudaMalloc(&h->ydev, out_bytes) != cudaSuccess) h->ydev = nullptr;
-    if (!h->xdev || !h->ydev) {
-      if (h->xdev) cudaFree(h->xdev);
-      h->xdev = nullptr;
-      cudaGetLastError();
-      return fail(h, TSF_ERR_NOMEM, "staging cudaMalloc failed");
-    }
+  tsf_status s = host_slot(h, &h->xdev, &h->ydev, in_bytes, out_bytes);
+  if (s == TSF_OK && n > 1) s = host_slot(h, &h->xdev2, &h->ydev2, in_bytes, out_bytes);
+  if (s != TSF_OK) return s;
+  if (!h->copy_stream) {
+    TSF_CUDA(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+    TSF_CUDA(h, cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking));
+    h->ev_h.resize(HOST_CHUNKS + 1 + 6);
+    for (auto& e : h->ev_h) TSF_CUDA(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   cudaStream_t st = (cudaStream_t)stream;
-  {
-    StageTimer tm(h, st, 3);
-    TSF_CUDA(h, cudaMemcpyAsync(h->xdev, x_host, in_bytes, cudaMemcpyHostToDevice, st));
-    tm.done();
-  }
-  if (P == 1 && h->K >= 2) {
-    // temporal stage whole (it needs every frame of a token), then the spatial
-    // stage in frame chunks: chunk c's y goes to the host on copy_stream while
-    // chunk c+1 computes (y is frame-major, so a chunk is contiguous)
-    if (!h->copy_stream) {
-      TSF_CUDA(h, cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
-      h->ev_h.resize(HOST_CHUNKS + 1);
-      for (auto& e : h->ev_h) TSF_CUDA(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
-    h->launches = 0;
-    const __nv_bfloat16* xd = h->xdev;
-    tsf_status s;
+  cudaEvent_t* ev_chunk = h->ev_h.data();                 // [HOST_CHUNKS]
+  cudaEvent_t ev_done = h->ev_h[HOST_CHUNKS];
+  cudaEvent_t* ev_in = h->ev_h.data() + HOST_CHUNKS + 1;  // [2] x of slot b on the device
+  cudaEvent_t* ev_used = ev_in + 2;                       // [2] the block has read x of slot b
+  cudaEvent_t* ev_out = ev_in + 4;                        // [2] y of slot b is on the host
+  // Pipeline over two device slots (item i uses slot i & 1):
+  //   h2d_stream:  H2D x_i  (after the block of item i-2 has read the slot)
+  //   stream:      block i  (after H2D x_i and after D2H y_{i-2} has drained the slot)
+  //   copy_stream: D2H y_i  (single GPU: per frame chunk, as soon as the chunk is computed)
+  // so H2D of item i+1 and D2H of item i run concurrently in the two PCIe directions and
+  // the blocks hide behind them.  Every cross-stream wait is issued right after the record
+  // it refers to, so reusing the events across items is exact.
+  TSF_CUDA(h, cudaEventRecord(ev_done, st));              // prior work on `stream` before any staging reuse
+  TSF_CUDA(h, cudaStreamWaitEvent(h->h2d_stream, ev_done, 0));
+  TSF_CUDA(h, cudaStreamWaitEvent(h->copy_stream, ev_done, 0));
+  for (int i = 0; i < n; ++i) {
+    const int b = i & 1;
+    __nv_bfloat16* xd = b ? h->xdev2 : h->xdev;
+    float* yd = b ? h->ydev2 : h->ydev;
+    if (i >= 2) TSF_CUDA(h, cudaStreamWaitEvent(h->h2d_stream, ev_used[b], 0));
     {
-      StageTimer tm(h, st, 0);
-      s = run_attention(h, temporal_view(h->K, h->N, h->H, h->d), xd, xd, xd, EPI_BLOCK_T, h->xt, nullptr, st);
+      StageTimer tm(h, h->h2d_stream, 3);
+      TSF_CUDA(h, cudaMemcpyAsync(xd, x_host[i], in_bytes, cudaMemcpyHostToDevice, h->h2d_stream));
       tm.done();
-      if (s != TSF_OK) return s;
     }
-    const int nch = h->K < HOST_CHUNKS ? h->K : HOST_CHUNKS;
-    const size_t frame = (size_t)h->N * h->H * h->d;
-    int f0 = 0;
-    for (int c = 0; c < nch; ++c) {
-      const int f1 = (int)(((long long)h->K * (c + 1)) / nch);
+    TSF_CUDA(h, cudaEventRecord(ev_in[b], h->h2d_stream));
+    TSF_CUDA(h, cudaStreamWaitEvent(st, ev_in[b], 0));
+    if (i >= 2) TSF_CUDA(h, cudaStreamWaitEvent(st, ev_out[b], 0));
+    if (P == 1 && h->K >= 2) {
+      // temporal stage whole (it needs every frame of a token), then the spatial
+      // stage in frame chunks: chunk c's y goes to the host on copy_stream while
+      // chunk c+1 computes (y is frame-major, so a chunk is contiguous)
+      h->launches = 0;
       {
-        StageTimer tm(h, st, 1);
-        s = run_attention(h, spatial_view(f1 - f0, h->N, h->H, h->d), h->xt + f0 * frame, h->xt + f0 * frame,
-                          h->xt + f0 * frame, EPI_BLOCK_S, nullptr, h->ydev + f0 * frame, st);
+        StageTimer tm(h, st, 0);
+        s = run_attention(h, temporal_view(h->K, h->N, h->H, h->d), xd, xd, xd, EPI_BLOCK_T, h->xt, nullptr, st);
         tm.done();
         if (s != TSF_OK) return s;
       }
-      TSF_CUDA(h, cudaEventRecord(h->ev_h[c], st));
-      TSF_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_h[c], 0));
-      TSF_CUDA(h, cudaMemcpyAsync(y_host + f0 * frame, h->ydev + f0 * frame, (f1 - f0) * frame * sizeof(float),
-                                  cudaMemcpyDeviceToHost, h->copy_stream));
-      f0 = f1;
+      TSF_CUDA(h, cudaEventRecord(ev_used[b], st));
+      const int nch = h->K < HOST_CHUNKS ? h->K : HOST_CHUNKS;
+      const size_t frame = (size_t)h->N * h->H * h->d;
+      int f0 = 0;
+      for (int c = 0; c < nch; ++c) {
+        const int f1 = (int)(((long long)h->K * (c + 1)) / nch);
+        {
+          StageTimer tm(h, st, 1);
+          s = run_attention(h, spatial_view(f1 - f0, h->N, h->H, h->d), h->xt + f0 * frame, h->xt + f0 * frame,
+                            h->xt + f0 * frame, EPI_BLOCK_S, nullptr, yd + f0 * frame, st);
+          tm.done();
+          if (s != TSF_OK) return s;
+        }
+        TSF_CUDA(h, cudaEventRecord(ev_chunk[c], st));
+        TSF_CUDA(h, cudaStreamWaitEvent(h->copy_stream, ev_chunk[c], 0));
+        TSF_CUDA(h, cudaMemcpyAsync(y_host[i] + f0 * frame, yd + f0 * frame, (f1 - f0) * frame * sizeof(float),
+                                    cudaMemcpyDeviceToHost, h->copy_stream));
+        f0 = f1;
+      }
+    } else {
+      s = tsf_spacetime_block(h, reinterpret_cast<const tsf_bf16*>(xd), yd, st);
+      if (s != TSF_OK) return s;
+      TSF_CUDA(h, cudaEventRecord(ev_used[b], st));
+      TSF_CUDA(h, cudaStreamWaitEvent(h->copy_stream, ev_used[b], 0));
+      StageTimer tm(h, h->copy_stream, 3);
+      TSF_CUDA(h, cudaMemcpyAsync(y_host[i], yd, out_bytes, cudaMemcpyDeviceToHost, h->copy_stream));
+      tm.done();
     }
-    TSF_CUDA(h, cudaEventRecord(h->ev_h[HOST_CHUNKS], h->copy_stream));
-    TSF_CUDA(h, cudaStreamWaitEvent(st, h->ev_h[HOST_CHUNKS], 0));  // the next call's stage buffers
-    return tsf_sync(h, st, 0);
+    TSF_CUDA(h, cudaEventRecord(ev_out[b], h->copy_stream));
   }
-  tsf_status s = tsf_spacetime_block(h, reinterpret_cast<const tsf_bf16*>(h->xdev), h->ydev, stream);
-  if (s != TSF_OK) return s;
-  {
-    StageTimer tm(h, st, 3);
-    TSF_CUDA(h, cudaMemcpyAsync(y_host, h->ydev, out_bytes, cudaMemcpyDeviceToHost, st));
-    tm.done();
-  }
+  TSF_CUDA(h, cudaEventRecord(ev_done, h->copy_stream));
+  TSF_CUDA(h, cudaStreamWaitEvent(st, ev_done, 0));       // `stream` completes after the last D2H
+  TSF_CUDA(h, cudaEventRecord(ev_in[0], h->h2d_stream));  // ... and after the last H2D (the next call's slots)
+  TSF_CUDA(h, cudaStreamWaitEvent(st, ev_in[0], 0));
   return tsf_sync(h, st, 0);
+}
+
+tsf_status tsf_spacetime_block_host(tsf_handle* h, const tsf_bf16* x_host, float* y_host, void* stream) {
+  if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
+  if (!x_host || !y_host) return fail(h, TSF_ERR_CONFIG, "null host buffer");
+  return tsf_spacetime_block_host_batch(h, &x_host, &y_host, 1, stream);
 }
 
 tsf_status tsf_sync(tsf_handle* h, void* stream, int timeout_ms) {

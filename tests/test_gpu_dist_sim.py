@@ -85,6 +85,23 @@ def test_sim_block_bitwise_equals_single_gpu(tsf_lib, single_cache, P, shape, mo
     sim.close()
 
 
+def test_sim_block_host_batch_equals_device_call(tsf_lib):
+    """The pipelined host batch on a (simulated) distributed handle: its generic
+    branch (whole block, one D2H per item) == the device call, bitwise."""
+    K, N, H, d, P = 8, 256, 2, 64, 2
+    sim = tsf_lib.Layer(K, N, H, d, sim_world=P)
+    xs = [synth.bits_to_torch(stack_token_shards(synth.make_x(K, N, H, d, seed=90 + i), P)) for i in range(3)]
+    want = []
+    for x in xs:
+        want.append(sim.block(x.cuda()).cpu())
+    sim.sync()
+    yh = [torch.empty(sim.frame_shard_shape, dtype=torch.float32).pin_memory() for _ in xs]
+    sim.block_host_batch([x.pin_memory() for x in xs], yh)
+    for i in range(3):
+        assert torch.equal(yh[i], want[i]), f"item {i}"
+    sim.close()
+
+
 @pytest.mark.parametrize("P,shape", [(2, (8, 64, 2, 64)), (4, (8, 96, 3, 32)), (8, (16, 64, 2, 128))])
 def test_sim_reshard_is_the_index_permutation(tsf_lib, P, shape):
     """I10: T2S equals oracle.reshard_t2s of the token shards; S2T o T2S = id (bitwise)."""

@@ -189,6 +189,27 @@ def test_block_host_api_matches_device_api(tsf_lib, shape):
     assert torch.equal(y_dev.cpu(), yh)
 
 
+@pytest.mark.parametrize("shape", [(8, 300, 2, 64), (1, 200, 2, 32), (3, 64, 2, 128)])
+@pytest.mark.parametrize("n", [1, 2, 5])
+def test_block_host_batch_matches_device_api(tsf_lib, shape, n):
+    """tsf_spacetime_block_host_batch (two device slots, H2D / block / D2H on three
+    streams): every item's y == the device call on that item's x, bitwise; distinct
+    inputs per item so a slot mix-up shows; a second batch on the same handle reuses
+    the slots."""
+    K, N, H, d = shape
+    layer = tsf_lib.Layer(K, N, H, d)
+    xbs = [synth.make_x(K, N, H, d, seed=30 + i) for i in range(n)]
+    want = [layer.block(to_dev(xb)).cpu() for xb in xbs]
+    xh = [synth.bits_to_torch(xb).pin_memory() for xb in xbs]
+    for rep in range(2):
+        yh = [torch.full((K, N, H, d), float("nan")).pin_memory() for _ in range(n)]
+        layer.block_host_batch(xh, yh)
+        for i in range(n):
+            assert torch.equal(yh[i], want[i]), f"batch {rep} item {i}"
+    assert layer.block_host_batch([], []) == []
+    assert tsf_lib.lib().tsf_spacetime_block_host_batch(layer._h, None, None, 2, None) == tsf_lib.TSF_ERR_CONFIG
+
+
 def test_transpose_is_exact_permutation(tsf_lib):
     K, N, H, d = 6, 130, 2, 64
     xb = synth.make_x(K, N, H, d, seed=9)
