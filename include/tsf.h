@@ -150,8 +150,12 @@ tsf_status tsf_full_block(tsf_handle* h, const tsf_block_weights* w, const tsf_b
  * P is recomputed (a forward pass that also yields the row statistics), then
  * one kernel per 128-key tile accumulates dk, dv in TMEM and adds dq into an
  * fp32 buffer.  All tensors bf16 [K, N, H, d]; fp32 accumulation; outputs must
- * not overlap inputs or each other.  d in {32, 64} (TSF_ERR_UNSUPPORTED for
- * d = 128); single-GPU handles.  Workspace allocated on first use. */
+ * not overlap inputs or each other.  d in {32, 64, 128}.  On a distributed
+ * (or simulated) handle the call acts on the rank's own shard, like the
+ * forward stage calls: temporal on the token shard [K, N/P, H, d], spatial on
+ * the frame shard [K/P, N, H, d]; no exchange.  dq is summed with fp32 atomic
+ * adds across key tiles, so results can differ run to run in the last bits
+ * (G22).  Workspace allocated on first use. */
 tsf_status tsf_temporal_attn_bwd(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v,
                                  const tsf_bf16* dO, tsf_bf16* dq, tsf_bf16* dk, tsf_bf16* dv, void* stream);
 tsf_status tsf_spatial_attn_bwd(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, const tsf_bf16* v,
