@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libtsf.so")
 SOURCES = [os.path.join(HERE, "csrc", "tsf.cu")]
 HEADERS = [os.path.join(HERE, "csrc", f) for f in ("sm100.cuh", "attn_common.cuh", "attn_packed.cuh",
-                                                   "attn_flash.cuh", "layout.cuh", "attn_stream.cuh", "attn_flash3.cuh", "gemm.cuh", "attn_bwd.cuh")] + \
+                                                   "attn_flash.cuh", "layout.cuh", "attn_stream.cuh", "attn_smallt.cuh", "attn_flash3.cuh", "gemm.cuh", "attn_bwd.cuh")] + \
     [os.path.join(ROOT, "include", "tsf.h")]
 
 

@@ -21,6 +21,7 @@
 #include "attn_flash.cuh"
 #include "attn_packed.cuh"
 #include "attn_stream.cuh"
+#include "attn_smallt.cuh"
 #include "attn_flash3.cuh"
 #include "gemm.cuh"
 #include "attn_bwd.cuh"
@@ -365,6 +366,17 @@ static bool use_stream(int d, int win) {
   return env != 0 && (d == 32 || d == 64) && (win == 32 || win == 64);
 }
 
+// Short-window temporal kernel (attn_smallt.cuh): d = 64, K in {4, 8, 16, 32}.
+// TSF_SMALLT=0 selects the tcgen05 stream kernel instead (A/B measurements).
+static bool use_smallt(int d, int L) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("TSF_SMALLT");
+    env = e ? atoi(e) : 1;
+  }
+  return env != 0 && d == 64 && (L == 4 || L == 8 || L == 16 || L == 32);
+}
+
 // TMEM slots of the stream kernel: TSF_STREAM_SLOTS = 2 | 4.  Four slots (S, P, O
 // aliased in 128 columns) measured no faster at C2 (34.7 vs 34.3 us, profiles/r07/traces,
 // trace 1831 vs 1773 cycles per tile): the stage is not limited by tiles in flight.
@@ -558,6 +570,70 @@ static tsf_status run_attention(tsf_handle* h, const View& v, const void* q, con
   p.dO = h->st_dO;
   p.lse_pitch = h->st_pitch;
   const bool packed = v.L <= 128 && !special;
+  if (packed && epi == EPI_BLOCK_T && use_smallt(d, v.L) && v.sB == (long long)v.A * v.sA && v.sA == d) {
+    // 256-row tiles of G = 256 / L whole groups (Ab heads x Bb tokens), every warp
+    // unit (16 or 32 rows) either fully inside the tile or skipped
+    const int G = 256 / v.L;
+    int Ab = 1;
+    for (int a = 1; a <= G && a <= v.A; ++a)
+      if (v.A % a == 0) Ab = a;
+    int Bb = G / Ab;
+    if (Bb > v.B) Bb = v.B;
+    const int unit = v.L < 16 ? 16 : v.L;
+    if ((Ab * Bb * v.L) % unit == 0) {
+      p.Ab = Ab; p.Bb = Bb;
+      p.tiles_a = v.A / Ab;
+      const long long tiles = (long long)p.tiles_a * ((v.B + Bb - 1) / Bb);
+      if (tiles > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "too many tiles");
+      p.num_tiles = (int)tiles;
+      CUtensorMap mx, mo;
+      memset(&mo, 0, sizeof mo);
+      tsf_status s;
+      if ((s = make_map(h, &mx, q, d, v, v.L, Ab, Bb, false)) != TSF_OK) return s;
+      if (dist) {
+        for (int r = 0; r < dist->P; ++r) {
+          const View pv{dist->Kc, v.A, dist->Nl, p.osL, p.osA, p.osB};
+          const void* base = static_cast<const __half*>(dist->peers[r]) + (size_t)dist->rank * dist->Nl * h->H * d;
+          if ((s = make_map(h, &h->pm.m[r], base, d, pv, dist->Kc, Ab, Bb, true)) != TSF_OK) return s;
+        }
+      } else if ((s = make_map(h, &mo, o, d, *ov, v.L, Ab, Bb, true)) != TSF_OK) {
+        return s;
+      }
+      if (getenv("TSF_SMALLT_NOMATH")) p.flags |= SMALLT_NO_MATH;
+      int grid = h->num_sms;
+      if (grid > p.num_tiles) grid = p.num_tiles;
+      static int warps = -1, bulk = -1;
+      if (warps < 0) {
+        const char* e = getenv("TSF_SMALLT_WARPS");
+        warps = (e && atoi(e) == 8) ? 8 : 16;
+        e = getenv("TSF_SMALLT_BULK");
+        bulk = e ? atoi(e) != 0 : 0;
+      }
+      // (the output's groups must be contiguous per frame too: X_t [K, N, H, d] or the
+      // peers' frame shards)
+      const bool use_bulk = bulk && (dist || (ov->sA == d && ov->sB == (long long)v.A * d));
+      if (use_bulk) {
+        // tiles of G consecutive groups of the frame plane, one 1-D copy per frame
+        const long long nt = ((long long)v.A * v.B + G - 1) / G;
+        if (nt > 0x7fffffffLL) return fail(h, TSF_ERR_CONFIG, "too many tiles");
+        p.num_tiles = (int)nt;
+        p.Ab = G; p.Bb = 1;  // (gt = G: every unit of a full tile is valid)
+        grid = h->num_sms < p.num_tiles ? h->num_sms : p.num_tiles;
+      }
+#define TSF_SMALLT_LAUNCH(LL, WW, BB)                                                                        \
+  launch(h, attn_smallt_kernel<LL, WW, BB>, grid, SmallTCfg<LL, WW, BB>::THREADS, SmallTCfg<LL, WW, BB>::SMEM, st, p, \
+         mx, mo, h->pm)
+#define TSF_SMALLT_W(LL, BB) (warps == 8 ? TSF_SMALLT_LAUNCH(LL, 8, BB) : TSF_SMALLT_LAUNCH(LL, 16, BB))
+      switch (v.L) {
+        case 4: return use_bulk ? TSF_SMALLT_W(4, true) : TSF_SMALLT_W(4, false);
+        case 8: return use_bulk ? TSF_SMALLT_W(8, true) : TSF_SMALLT_W(8, false);
+        case 16: return use_bulk ? TSF_SMALLT_W(16, true) : TSF_SMALLT_W(16, false);
+        default: return use_bulk ? TSF_SMALLT_LAUNCH(32, 8, true) : TSF_SMALLT_LAUNCH(32, 8, false);
+      }
+#undef TSF_SMALLT_W
+#undef TSF_SMALLT_LAUNCH
+    }
+  }
   p.mask_mode = mask;
   p.mask_n = h->N;
   if (!kvv) kvv = &v;  // keys / values: the query view unless cross-attention

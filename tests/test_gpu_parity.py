@@ -347,3 +347,40 @@ def test_c_abi_program(tsf_lib, tmp_path):
     assert r.returncode == 0, r.stderr
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "C ABI OK" in r.stdout, r.stdout + r.stderr
+
+
+# Short-window temporal kernel (attn_smallt.cuh, d = 64, K in {4, 8, 16, 32}):
+# 256-row tiles of 256 / K whole groups; G_tot = N * H groups per frame.
+SMALLT_SHAPES = [
+    (8, 301, 1, 64),     # 301 groups: last tile 13 groups (odd at K = 8 -> zero-filled pair partner)
+    (4, 333, 3, 64),     # K = 4: 999 groups, last tile 39 (a unit of 4 groups, 3 valid)
+    (16, 77, 3, 64),     # K = 16: 231 groups, tiles of 16, last 7
+    (32, 45, 2, 64),     # K = 32 (two m-tiles per unit), 90 groups, tiles of 8, last 2
+    (8, 7, 1, 64),       # fewer groups than one tile
+]
+
+
+@pytest.mark.parametrize("shape", SMALLT_SHAPES)
+def test_block_short_window_temporal_ragged(tsf_lib, shape):
+    K, N, H, d = shape
+    xb = synth.make_x(K, N, H, d, seed=61)
+    layer = tsf_lib.Layer(K, N, H, d)
+    y = host(layer.block(to_dev(xb)))
+    layer.sync()
+    check(y, oracle.block(f64(xb)), f"short-window block {shape}")
+
+
+def test_block_short_window_after_nonfinite_input(tsf_lib):
+    """A non-finite x is reported; the next call on the same handle (same input
+    ring, odd last tile) is clean: no stale inf reaches it through 0 * inf."""
+    K, N, H, d = 8, 301, 1, 64
+    layer = tsf_lib.Layer(K, N, H, d)
+    bad = torch.full((K, N, H, d), float("inf"), dtype=torch.bfloat16, device="cuda")
+    layer.block(bad)
+    with pytest.raises(tsf_lib.TsfError) as e:
+        layer.sync()
+    assert e.value.status == tsf_lib.TSF_ERR_NUMERIC
+    xb = synth.make_x(K, N, H, d, seed=62)
+    y = host(layer.block(to_dev(xb)))
+    layer.sync()
+    check(y, oracle.block(f64(xb)), "short-window block after a non-finite call")
