@@ -544,6 +544,9 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
         // SEP: all of P_t is packed in registers and stored after the last
         // exponential, so the wait for PV_t(G-1) (P_t's buffer) is at the end
         uint32_t pk_all[C::SEP ? CW / 2 : 1];
+#ifdef TSF_FLASH_INPLACE_AB
+        // (A/B builds only: compiled in, this branch alone costs the default path
+        // stack frame and 13% of the C5 temporal stage)
         if (C::SEP && (p.flags & FLASH_INPLACE_EXP)) {
           // one dependency graph over all CW columns, transformed in place
           // (scores -> log2-domain exponents -> P -> packed pairs), so the
@@ -568,6 +571,7 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
             if constexpr (!C::ONES) { ls0 += f[c]; ls1 += f[c + 1]; }
           }
         } else
+#endif
 #pragma unroll
         for (int c0 = 0; c0 < CW; c0 += PW) {
           // three passes over PW columns (scale, exponentiate, pack) so no
@@ -763,34 +767,19 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
       };
       static_assert((SUB * 2 * D / 16 / 32) % 8 == 0, "conversion batching");
       int g = 0;
-      const bool skip = (p.flags & FLASH_NO_CONVERT) != 0;  // diagnostics: timing only, wrong results
-      // Q(k) is converted as soon as it has landed, between the K tiles of
-      // item k - 1, so the first QK^T of an item does not wait for the 32 KB Q
-      // conversion at the item boundary (C5 temporal stage: 12% of its time)
-      int q_conv_done = -1;  // last item whose Q tiles are converted
-      auto convert_q = [&](int kq) {
-        const int qs = kq % C::QST;
-        if (!skip) {
-          convert_tile(sQ + qs * C::Q_BYTES, 128);
-          convert_tile(sQ + qs * C::Q_BYTES + C::Q_TILE, 128);
-        }
-        if (lane == 0) mbar_arrive(&q_conv[qs]);
-        q_conv_done = kq;
-      };
+      // (converting the next item's Q between K tiles, instead of at the item
+      // boundary, measured neutral at C5 and perturbed the kernel's code: removed)
       for (int k = 0; k < my_items; ++k) {
-        if (q_conv_done < k) {
-          mbar_wait(&q_full[k % C::QST], (k / C::QST) & 1);
-          convert_q(k);
-        }
+        const int qs = k % C::QST;
+        mbar_wait(&q_full[qs], (k / C::QST) & 1);
+        convert_tile(sQ + qs * C::Q_BYTES, 128);
+        convert_tile(sQ + qs * C::Q_BYTES + C::Q_TILE, 128);
+        if (lane == 0) mbar_arrive(&q_conv[qs]);
         for (int j = 0; j < nkv; ++j, ++g) {
           const int s = g % NST;
           mbar_wait(&k_full[s], (g / NST) & 1);
-          if (!skip) convert_tile(sKV + s * C::STAGE_BYTES, SUB);
+          convert_tile(sKV + s * C::STAGE_BYTES, SUB);
           if (lane == 0) mbar_arrive(&kv_conv[s]);
-          const int kn = k + 1;
-          if (q_conv_done < kn && kn < my_items &&
-              __any_sync(0xffffffffu, mbar_test(&q_full[kn % C::QST], (kn / C::QST) & 1)))  // warp-uniform
-            convert_q(kn);
         }
       }
     }
