@@ -391,7 +391,15 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
     const uint32_t tOrow = tmem + lane_base + (t ? C::COL_O1 : C::COL_O0);
     constexpr int OCOLS = D / SPLIT;                           // O columns this warp rescales / stores
     const float sl2 = p.scale_log2;
+#ifdef TSF_FLASH_PINGPONG_AB
     const bool pingpong = (p.flags & FLASH_PINGPONG) != 0;
+#else
+    // ping-pong (measured no faster) is compiled in only for A/B builds: its
+    // bar.arrive sits between the exponentials and the P store, and even never
+    // taken, that asm (a memory clobber) constrains the scheduling of every
+    // step (C2 spatial 690 -> 727 us with it compiled in, profiles/r07/c5_regression)
+    constexpr bool pingpong = false;
+#endif
     int G0 = 0;  // global KV tile index of the item's first tile
     for (int k = 0; k < my_items; ++k, G0 += nkv) {
       int qp, ga, gb;
