@@ -205,6 +205,9 @@ tsf_status tsf_spacetime_block_host(tsf_handle* h, const tsf_bf16* x_host, float
  * synchronised (all y_host written); host buffers must stay valid until then.
  * Each y_host[i] is bitwise what tsf_spacetime_block_host gives for
  * x_host[i].  n = 0 is a no-op; a null array or element is TSF_ERR_CONFIG.
+ * On any error the call returns only after the copies it queued have drained
+ * (the host buffers are free again); a non-finite X_t in any item is
+ * TSF_ERR_NUMERIC, as for tsf_spacetime_block_host.
  * Collective on distributed handles (every rank passes the same n). */
 tsf_status tsf_spacetime_block_host_batch(tsf_handle* h, const tsf_bf16* const* x_host, float* const* y_host, int n,
                                           void* stream);

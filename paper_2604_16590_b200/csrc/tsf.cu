@@ -1830,8 +1830,8 @@ static tsf_status host_slot(tsf_handle* h, __nv_bfloat16** x, float** y, size_t 
   return TSF_OK;
 }
 
-tsf_status tsf_spacetime_block_host_batch(tsf_handle* h, const tsf_bf16* const* x_host, float* const* y_host, int n,
-                                          void* stream) {
+static tsf_status host_batch_enqueue(tsf_handle* h, const tsf_bf16* const* x_host, float* const* y_host, int n,
+                                     void* stream) {
   if (!h) return fail(nullptr, TSF_ERR_CONFIG, "null handle");
   if (n < 0 || (n > 0 && (!x_host || !y_host))) return fail(h, TSF_ERR_CONFIG, "need n >= 0 and pointer arrays");
   for (int i = 0; i < n; ++i)
@@ -1925,6 +1925,19 @@ tsf_status tsf_spacetime_block_host_batch(tsf_handle* h, const tsf_bf16* const* 
   TSF_CUDA(h, cudaEventRecord(ev_in[0], h->h2d_stream));  // ... and after the last H2D (the next call's slots)
   TSF_CUDA(h, cudaStreamWaitEvent(st, ev_in[0], 0));
   return tsf_sync(h, st, 0);
+}
+
+tsf_status tsf_spacetime_block_host_batch(tsf_handle* h, const tsf_bf16* const* x_host, float* const* y_host, int n,
+                                          void* stream) {
+  const tsf_status s = host_batch_enqueue(h, x_host, y_host, n, stream);
+  if (s != TSF_OK && h) {
+    // an error mid-batch: copies already queued on the two copy streams may still
+    // read x_host / write y_host -- drain them before the caller gets control back
+    if (h->h2d_stream) cudaStreamSynchronize(h->h2d_stream);
+    if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
+    cudaGetLastError();
+  }
+  return s;
 }
 
 tsf_status tsf_spacetime_block_host(tsf_handle* h, const tsf_bf16* x_host, float* y_host, void* stream) {

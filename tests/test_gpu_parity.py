@@ -207,6 +207,15 @@ def test_block_host_batch_matches_device_api(tsf_lib, shape, n):
         for i in range(n):
             assert torch.equal(yh[i], want[i]), f"batch {rep} item {i}"
     assert layer.block_host_batch([], []) == []
+    if n == 2 and shape[0] == 8:
+        # one non-finite item: TSF_ERR_NUMERIC for the batch, then a clean batch on the handle
+        bad = [xh[0], torch.full_like(xh[1], float("inf")).pin_memory()]
+        with pytest.raises(tsf_lib.TsfError) as e:
+            layer.block_host_batch(bad, [torch.empty_like(want[0]).pin_memory() for _ in range(2)])
+        assert e.value.status == tsf_lib.TSF_ERR_NUMERIC
+        yh = [torch.empty_like(want[0]).pin_memory() for _ in range(n)]
+        layer.block_host_batch(xh, yh)
+        assert all(torch.equal(yh[i], want[i]) for i in range(n))
     assert tsf_lib.lib().tsf_spacetime_block_host_batch(layer._h, None, None, 2, None) == tsf_lib.TSF_ERR_CONFIG
 
 
