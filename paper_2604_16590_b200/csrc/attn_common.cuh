@@ -100,10 +100,9 @@ struct AttnParams {
   const void* dO;
   int lse_pitch;
 };
-constexpr int FLASH_PINGPONG = 2;
+constexpr int FLASH_PINGPONG = 2;     // (builds with -DTSF_FLASH_PINGPONG_AB only)
 constexpr int FLASH_RES_GLOBAL = 4;  // flash kernel: block residual from global memory, not the Q tile (diagnostics)
-constexpr int FLASH_INPLACE_EXP = 8; // flash kernel (SEP): the exponential phase as one in-place pass over the row
-constexpr int FLASH_NO_CONVERT = 16; // diagnostics: skip the bf16 -> fp16 conversion (timing only, wrong results)
+constexpr int FLASH_INPLACE_EXP = 8; // flash kernel (SEP), builds with -DTSF_FLASH_INPLACE_AB only: the exponential phase as one in-place pass over the row
 
 constexpr int MAX_PEERS = 8;
 // per-destination output tensor maps (packed kernel, distributed temporal stage)

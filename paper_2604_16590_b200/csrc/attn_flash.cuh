@@ -118,7 +118,13 @@ attn_flash_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant_
   // (block temporal stage: the Q tile holds fp16(x), converted in place; equal
   // to the bf16 x except below 2^-14 in magnitude, where it differs by < 2^-25)
   constexpr bool RES_SMEM_OK = C::SEP && EPI != EPI_OUT16;
+#ifdef TSF_FLASH_RESGLOBAL_AB
   const bool RES_SMEM = RES_SMEM_OK && !(p.flags & FLASH_RES_GLOBAL);
+#else
+  // (the global-residual diagnostic is compiled in only for A/B builds: its
+  // prefetch branch sits in the step loop)
+  constexpr bool RES_SMEM = RES_SMEM_OK;
+#endif
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                        // QST x (Q0 | Q1)
