@@ -1056,7 +1056,26 @@ tsf_status tsf_joint_attn(tsf_handle* h, const tsf_bf16* q, const tsf_bf16* k, c
   // all K*N tokens as one sequence per head: [K, N, H, d] = [1, K*N, H, d]
   const View jv{h->K * h->N, h->H, 1, (long long)h->H * h->d, (long long)h->d, (long long)h->K * h->N * h->H * h->d};
   StageTimer tm(h, st, 5);
-  s = run_attention(h, jv, q, k, v, EPI_OUT16, o, nullptr, st, nullptr, nullptr, mask);
+  static int split = -1;
+  if (split < 0) {
+    const char* e = getenv("TSF_CAUSAL_SPLIT");
+    split = e ? atoi(e) != 0 : 1;
+  }
+  if (mask == TSF_MASK_CAUSAL_FRAMES && split && h->N > 128) {
+    // causal frames [t' <= t]: the queries of frame t attend exactly to the first
+    // (t + 1) N tokens, so frame t is an unmasked attention of its N queries over
+    // that key prefix -- K launches doing K (K + 1) / 2 frames of keys instead of
+    // one masked launch visiting all K^2 (the flash kernel's separate key length)
+    const size_t frame = (size_t)h->N * h->H * h->d;
+    const View qv{h->N, h->H, 1, (long long)h->H * h->d, (long long)h->d, (long long)frame};
+    for (int t = 0; t < h->K && s == TSF_OK; ++t) {
+      const View kv{(t + 1) * h->N, h->H, 1, (long long)h->H * h->d, (long long)h->d, (long long)h->K * frame};
+      s = run_attention(h, qv, reinterpret_cast<const __nv_bfloat16*>(q) + t * frame, k, v, EPI_OUT16,
+                        reinterpret_cast<__nv_bfloat16*>(o) + t * frame, nullptr, st, nullptr, nullptr, 0, &kv);
+    }
+  } else {
+    s = run_attention(h, jv, q, k, v, EPI_OUT16, o, nullptr, st, nullptr, nullptr, mask);
+  }
   tm.done();
   return s;
 }

@@ -28,7 +28,8 @@ def check(got, want, what):
 
 
 @pytest.mark.parametrize("shape", [(4, 64, 2, 32), (3, 100, 2, 64), (2, 200, 1, 128), (5, 20, 2, 64),
-                                   (6, 50, 3, 64), (1, 130, 2, 64)])
+                                   (6, 50, 3, 64), (1, 130, 2, 64),
+                                   (4, 257, 2, 64), (3, 300, 2, 32)])   # causal: per-frame key prefixes
 @pytest.mark.parametrize("mask", [0, 1, 2, 3])
 def test_joint_matches_oracle(tsf_lib, shape, mask):
     K, N, H, d = shape
