@@ -15,7 +15,8 @@
 //   thread 0      keeps NS = 4 x 32 KB input tiles in flight (one 4-D TMA
 //                 box per tile: d x K frames x Ab x Bb groups, SWIZZLE_128B,
 //                 group-major rows) and issues the tile's output TMA store(s)
-//   warps 0-7     per 16-row m-tile: ldmatrix x -> registers, bf16 -> fp16
+//   warps         16 for K <= 16 (one 16-row unit each per tile), 8 for K = 32
+//                 (one 32-row group each); per 16-row m-tile: ldmatrix x -> registers, bf16 -> fp16
 //                 (exact for |x| < 65504), S = X X^T with mma.sync m16n8k16
 //                 (fp32 accumulate; the key fragments ARE the query
 //                 fragments, q = k = v = x), block-diagonal softmax in
@@ -29,6 +30,10 @@
 // MMA is the right unit here: the tensor pipe is < 5% busy either way and
 // what matters is that no role waits on another (K-small
 // temporal kernel).
+//
+// Variants (A/B, profiles/r07/smallt): TSF_SMALLT_WARPS=8; TSF_SMALLT_BULK=1
+// (1-D bulk copies per frame into a padded frame-major ring instead of the
+// 4-D boxes: slower, 33 vs 31 us at C2 and 0.95 vs 0.54 ms at C3).
 //
 // Rows of a tile: group-major, row R = gi * L + l (gi = bb * Ab + ab, l the
 // frame).  A warp unit is 16 rows (L <= 16: 16 / L whole groups, block-
