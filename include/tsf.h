@@ -49,7 +49,7 @@ typedef enum {
   TSF_ERR_NUMERIC = 3,     /* non-finite block intermediate X_t (fp16 overflow or non-finite x), see tsf_sync */
   TSF_ERR_UNSUPPORTED = 4, /* d not in {32, 64, 128}, or device is not sm_100 */
   TSF_ERR_CUDA = 5,        /* CUDA runtime/driver failure (launch, copy, tensor map) */
-  TSF_ERR_NCCL = 6,        /* NCCL failure */
+  TSF_ERR_NCCL = 6,        /* NCCL failure, or a peer rank stopped (fused-exchange barrier timeout) */
   TSF_ERR_NOMEM = 7        /* workspace allocation failed */
 } tsf_status;
 

@@ -70,6 +70,12 @@ struct tsf_handle {
   std::vector<cudaEvent_t> ev_f;         // [fchunks + 1]
   bool fused = false;
   int* d_flag = nullptr;        // 1-int NCCL all-reduce = cross-rank barrier
+  // peer-memory barrier of the fused exchange (TSF_PEER_BARRIER, default on):
+  // a 1 KB flag area after each rank's ubuf[0] (IPC-mapped with it); rank r's
+  // slot s holds the epoch rank s last announced to r
+  unsigned int* peer_flags[MAX_PEERS] = {};
+  unsigned int bar_epoch = 0;
+  bool peer_barrier = false;
   PeerMaps pm{};                // per-destination output maps of the current launch
   bool use_pm = false;
   // host API (single GPU): the spatial stage runs in frame chunks and each
@@ -746,6 +752,11 @@ static tsf_status check_shape(int K, int N, int H, int d, int world) {
   return TSF_OK;
 }
 
+// flag area of the peer barrier: 1 KB after a frame-shard buffer of El halves
+constexpr size_t FLAG_AREA_BYTES = 1024;
+static size_t flag_area_off(size_t El) { return (El * sizeof(__half) + 255) & ~size_t(255); }
+static size_t flag_area_halfs(size_t El) { return (flag_area_off(El) + FLAG_AREA_BYTES) / sizeof(__half); }
+
 static tsf_status alloc_workspace(tsf_handle* h) {
   // token-shard elements (times the virtual ranks of a simulated handle)
   const size_t El = (size_t)h->K * (h->N / h->world) * h->H * h->d * (h->sim ? h->world : 1);
@@ -753,15 +764,18 @@ static tsf_status alloc_workspace(tsf_handle* h) {
     return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(__half)) == cudaSuccess;
   };
   bool ok = a(&h->xt, El);
-  if (ok && h->world > 1) ok = a(&h->rxt, El) && a(&h->uxt, El);
+  if (ok && h->world > 1) ok = a(&h->rxt, El) && a(&h->uxt, h->sim ? El : flag_area_halfs(El));
+  if (ok && h->world > 1 && !h->sim)
+    ok = cudaMemset(reinterpret_cast<char*>(h->uxt) + flag_area_off(El), 0, FLAG_AREA_BYTES) == cudaSuccess;
   if (ok && h->world > 1 && !h->sim)
     ok = cudaMalloc(reinterpret_cast<void**>(&h->scratch), 256 + (size_t)h->world * 2 * sizeof(cudaIpcMemHandle_t)) ==
          cudaSuccess;
   if (ok) {
     unsigned int* hp = nullptr;
-    ok = cudaHostAlloc(reinterpret_cast<void**>(&hp), sizeof(unsigned int), cudaHostAllocMapped) == cudaSuccess;
+    // [0] non-finite X_t, [1] peer-barrier timeout
+    ok = cudaHostAlloc(reinterpret_cast<void**>(&hp), 2 * sizeof(unsigned int), cudaHostAllocMapped) == cudaSuccess;
     if (ok) {
-      *hp = 0u;
+      hp[0] = hp[1] = 0u;
       h->nf_host = hp;
       ok = cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->nf_dev), hp, 0) == cudaSuccess;
     }
@@ -888,7 +902,7 @@ tsf_status tsf_create_dist(int K, int N, int H, int d, const void* id128, int ra
       h->ubuf[0] = h->uxt;
       cudaIpcMemHandle_t mine[2];
       memset(mine, 0, sizeof mine);
-      bool ok = cudaMalloc(reinterpret_cast<void**>(&h->ubuf[1]), El * sizeof(__half)) == cudaSuccess &&
+      bool ok = cudaMalloc(reinterpret_cast<void**>(&h->ubuf[1]), flag_area_halfs(El) * sizeof(__half)) == cudaSuccess &&
                 cudaIpcGetMemHandle(&mine[0], h->ubuf[0]) == cudaSuccess &&
                 cudaIpcGetMemHandle(&mine[1], h->ubuf[1]) == cudaSuccess;
       cudaGetLastError();
@@ -914,6 +928,13 @@ tsf_status tsf_create_dist(int K, int N, int H, int d, const void* id128, int ra
             if (h->peer_buf[b][p] && p != rank) cudaIpcCloseMemHandle(h->peer_buf[b][p]);
             h->peer_buf[b][p] = nullptr;
           }
+      }
+      if (fused) {
+        for (int p = 0; p < world; ++p)
+          h->peer_flags[p] =
+              reinterpret_cast<unsigned int*>(static_cast<char*>(h->peer_buf[0][p]) + flag_area_off(El));
+        const char* pb = getenv("TSF_PEER_BARRIER");
+        h->peer_barrier = !(pb && atoi(pb) == 0);
       }
       int fc = 1;
       if (const char* e = getenv("TSF_FUSED_CHUNKS")) fc = atoi(e);
@@ -1598,6 +1619,49 @@ tsf_status tsf_full_block(tsf_handle* h, const tsf_block_weights* w, const tsf_b
 // Temporal stage of rank `rank` with the fused exchange: X_t rows go straight
 // into every rank's frame shard (peers[r]); vin is the rank's token-shard view
 // (all heads, or one head chunk).
+// Cross-rank barrier of the fused exchange over peer memory (replaces the 1-int
+// NCCL all-reduce, ~16-36 us, on the step's critical path).  Thread r announces
+// `epoch` in peer r's slot for this rank (release, system scope: the temporal
+// kernel that stored X_t rows into the peers ran before this one on the
+// stream), then waits (acquire) until peer r has announced it here.  Bounded:
+// after ~10 s a missing peer sets err (host-mapped), reported by tsf_sync.
+struct PeerFlags {
+  unsigned int* f[MAX_PEERS];
+};
+__global__ void peer_barrier_kernel(const PeerFlags pf, int rank, int P, unsigned int epoch, unsigned int* err) {
+  const int r = threadIdx.x;
+  if (r < P) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pf.f[r] + rank), "r"(epoch) : "memory");
+  }
+  if (r < P) {
+    const unsigned int* mine = pf.f[rank] + r;
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+      unsigned int v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+      if ((int)(v - epoch) >= 0) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 10000000000ull) {  // 10 s
+        *reinterpret_cast<volatile unsigned int*>(err) = 1u;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+}
+
+static tsf_status peer_barrier(tsf_handle* h, cudaStream_t st) {
+  PeerFlags pf{};
+  for (int r = 0; r < h->world && r < MAX_PEERS; ++r) pf.f[r] = h->peer_flags[r];
+  peer_barrier_kernel<<<1, 32, 0, st>>>(pf, h->rank, h->world, ++h->bar_epoch, h->nf_dev + 1);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(h, TSF_ERR_CUDA, std::string("peer barrier launch: ") + cudaGetErrorString(e));
+  h->launches++;
+  return TSF_OK;
+}
+
 static tsf_status temporal_fused(tsf_handle* h, const View& vin, const tsf_bf16* x, int rank, void* const* peers,
                                  cudaStream_t st) {
   const DistOut dist{h->world, h->K / h->world, rank, h->N / h->world, peers};
@@ -1774,7 +1838,11 @@ tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void*
       s = temporal_fused(h, temporal_view(h->K, Nl, H, d), x, h->rank, peers, st);
       if (s == TSF_OK) {
         StageTimer tm(h, st, 2);
-        TSF_NCCL(h, ncclAllReduce(h->d_flag, h->d_flag, 1, ncclInt32, ncclSum, h->comm, st));
+        if (h->peer_barrier) {
+          if ((s = peer_barrier(h, st)) != TSF_OK) return s;
+        } else {
+          TSF_NCCL(h, ncclAllReduce(h->d_flag, h->d_flag, 1, ncclInt32, ncclSum, h->comm, st));
+        }
         tm.done();
         s = spatial_shard(h, u, y, 1, 0, false, st);
         if (s == TSF_OK) h->fparity ^= 1;
@@ -1988,6 +2056,10 @@ tsf_status tsf_sync(tsf_handle* h, void* stream, int timeout_ms) {
       }
     }
     if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  if (h->nf_host && h->nf_host[1]) {
+    h->nf_host[1] = 0u;
+    return fail(h, TSF_ERR_NCCL, "fused-exchange peer barrier timed out (a peer rank stopped)");
   }
   if (h->nf_host && *h->nf_host) {
     *h->nf_host = 0u;
