@@ -183,8 +183,12 @@ tsf_status tsf_spacetime_block_bwd(tsf_handle* h, const tsf_bf16* x, const float
  * tsf_sync (and by tsf_spacetime_block_host, which synchronises).  y is then
  * not meaningful.
  * Single GPU: x, y are [K, N, H, d].  Distributed: x is the token shard
- * [K, N/P, H, d], y the frame shard [K/P, N, H, d]; one all-to-all (NCCL,
- * bytes, bit-exact) reshards X_t between the stages. */
+ * [K, N/P, H, d], y the frame shard [K/P, N, H, d]; X_t is resharded between
+ * the stages bit-exactly: by default the temporal kernel stores its rows
+ * straight into the owning ranks' frame shards over NVLink (CUDA IPC) and a
+ * peer-memory barrier orders the stores before the spatial stage; NCCL byte
+ * send/recv plus an unpack kernel where that is unavailable
+ * (TSF_FUSED_EXCHANGE=0, or shapes the fused scatter does not cover). */
 tsf_status tsf_spacetime_block(tsf_handle* h, const tsf_bf16* x, float* y, void* stream);
 
 /* Same as tsf_spacetime_block with HOST buffers (pinned memory recommended):
@@ -219,6 +223,9 @@ tsf_status tsf_spacetime_block_host_batch(tsf_handle* h, const tsf_bf16* const* 
  *                    while waiting, or timeout_ms > 0 elapsed first: then the
  *                    communicator is aborted (a dead or hung peer cannot hang
  *                    this rank forever) and later collective calls on h fail;
+ *                    or the fused exchange's peer-memory barrier waited 10 s
+ *                    for a peer that never arrived (the ranks' barrier epochs
+ *                    are then out of step: destroy the handle);
  *   TSF_ERR_CUDA     the stream reported a CUDA error.
  * timeout_ms <= 0 waits without a limit.  Polls the stream (no blocking sync). */
 tsf_status tsf_sync(tsf_handle* h, void* stream, int timeout_ms);
