@@ -46,6 +46,15 @@ def cases():
             pytest.param(P, (128, 32 * P, 2, 128), id=f"P{P}-K128-d128"),        # C4-at-P=8 temporal shape
         ]
     out.append(pytest.param(4, (12, 96, 3, 32), id="P4-d32-ragged"))
+    # short-window temporal kernel (d = 64, K in {4, 8, 16, 32}) with K/P < 8 frames per
+    # rank: its per-destination staging sub-tiles of G * K/P rows (K/P = 4, 2, 1)
+    out += [
+        pytest.param(2, (8, 256, 2, 64), id="P2-smallt-Kc4"),
+        pytest.param(4, (8, 256, 2, 64), id="P4-smallt-Kc2"),
+        pytest.param(8, (8, 256, 2, 64), id="P8-smallt-Kc1"),
+        pytest.param(4, (16, 128, 3, 64), id="P4-smallt-K16-H3"),
+        pytest.param(4, (4, 64, 2, 64), id="P4-smallt-K4-Kc1"),
+    ]
     return out
 
 
